@@ -1,0 +1,379 @@
+// C ABI entry points (include/btk.h): validation, workspace planning and
+// dispatch between the fused interleaved kernel and the generic path.
+#include <cstring>
+
+#include "../../include/btk.h"
+#include "btk_internal.h"
+
+using namespace btk;
+
+namespace {
+
+thread_local int g_last_cuda = 0;
+
+int cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return BTK_OK;
+  g_last_cuda = (int)e;
+  return BTK_ERR_CUDA;
+}
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+size_t al(size_t v) { return (v + 255) & ~(size_t)255; }
+
+bool dtype_ok(int d) { return d == BTK_F32 || d == BTK_BF16 || d == BTK_F16; }
+
+int vbytes(int d) { return d == BTK_F32 ? 4 : 2; }
+
+CompGeo geo_for(int dtype, int64_t space) {
+  switch (dtype) {
+    case BTK_F32: return make_geo<F32>(space);
+    case BTK_BF16: return make_geo<BF16>(space);
+    default: return make_geo<F16>(space);
+  }
+}
+
+// Workspace carve-up of the generic path.
+struct Plan {
+  size_t pool = 0, mat = 0, s1a = 0, s1b = 0, s2a = 0, s2b = 0;
+  size_t total() const { return al(pool) + al(mat) + al(s1a) + al(s1b) + al(s2a) + al(s2b); }
+};
+
+Plan plan_generic(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb) {
+  Plan pl;
+  const int64_t s = ceil_div(n, b);
+  if (b == 1) {
+    pl.mat = (size_t)(m * n * 8);
+    if (n > K2_SMALL_CAP) pl.s2a = pl.s2b = (size_t)(m * kb * 8);
+    return pl;
+  }
+  pl.pool = (size_t)(m * b * kb * 8);
+  if (kb > 16) {
+    pl.mat = (size_t)(m * b * s * 8);
+    if (s > K2_SMALL_CAP) pl.s1a = pl.s1b = (size_t)(m * b * kb * 8);
+  }
+  if (b * kb > K2_SMALL_CAP) pl.s2a = pl.s2b = (size_t)(m * k * 8);
+  return pl;
+}
+
+struct Carve {
+  uint8_t* p;
+  uint64_t* take(size_t bytes) {
+    if (!bytes) return nullptr;
+    uint64_t* r = reinterpret_cast<uint64_t*>(p);
+    p += al(bytes);
+    return r;
+  }
+};
+
+// Stage 1 into the bucket-major pool (m x b*kb comps).
+int stage1_pool(const Problem& p, const Plan& pl, Carve& cv, uint64_t* pool, cudaStream_t st) {
+  if (p.kb <= 16) return cuda_status(run_stage1_generic(p, pool, st));
+  uint64_t* mat = cv.take(pl.mat);
+  uint64_t* s1a = cv.take(pl.s1a);
+  uint64_t* s1b = cv.take(pl.s1b);
+  int rc = cuda_status(run_materialize(p, mat, st));
+  if (rc) return rc;
+  K2Args a{};
+  a.in = mat;
+  a.in_stride = ceil_div(p.n, p.b);
+  a.nseg = p.m * p.b;
+  a.L = a.in_stride;
+  a.kk = p.kb;
+  a.out_keys = pool;
+  a.out_stride = p.kb;
+  a.geo = p.geo;
+  a.scratch_a = s1a;
+  a.scratch_b = s1b;
+  return cuda_status(run_k2(p.dtype, false, a, st));
+}
+
+int check_common(const void* x, int dtype, int layout, int64_t n, int64_t row_stride) {
+  if (!dtype_ok(dtype)) return BTK_ERR_DTYPE;
+  if (layout != BTK_INTERLEAVED && layout != BTK_CONTIGUOUS) return BTK_ERR_ASSIGNMENT;
+  if (n >= (int64_t(1) << 31)) return BTK_ERR_SHAPE;
+  if (row_stride < n) return BTK_ERR_SHAPE;
+  if (x == nullptr) return BTK_ERR_SHAPE;
+  if ((reinterpret_cast<uintptr_t>(x) % vbytes(dtype)) != 0) return BTK_ERR_ALIGNMENT;
+  return BTK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int btk_validate(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb) {
+  if (m < 1 || n < 1 || k < 1 || b < 1 || kb < 1) return BTK_ERR_NONPOSITIVE;
+  if (k > n) return BTK_ERR_K_GT_N;
+  if (b > n) return BTK_ERR_B_GT_N;
+  if (kb > std::min<int64_t>(k, ceil_div(n, b))) return BTK_ERR_KB_RANGE;
+  if (b * kb < k) return BTK_ERR_UNDERSAMPLED;
+  return BTK_OK;
+}
+
+int btk_stage1_validate(int64_t n, int64_t b, int64_t kb) {
+  if (n < 1) return BTK_ERR_SHAPE;
+  if (b < 1 || b > n) return BTK_ERR_B_GT_N;
+  if (kb < 1 || kb > ceil_div(n, b)) return BTK_ERR_KB_RANGE;
+  return BTK_OK;
+}
+
+int64_t btk_stage1_count(int64_t n, int64_t b, int64_t kb, int layout) {
+  if (btk_stage1_validate(n, b, kb) != BTK_OK) return -1;
+  const int64_t q = n / b, r = n % b;
+  if (kb <= q) return b * kb;
+  (void)layout;  // both layouts have r buckets of q+1 and b-r of q
+  return r * std::min<int64_t>(kb, q + 1) + (b - r) * std::min<int64_t>(kb, q);
+}
+
+size_t btk_workspace_bytes(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, int dtype,
+                           int layout) {
+  (void)dtype;
+  (void)layout;
+  if (btk_validate(m, n, k, b, kb) != BTK_OK) return 0;
+  return plan_generic(m, n, k, b, kb).total();
+}
+
+int btk_uses_fused_path(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, int dtype,
+                        int layout, int64_t row_stride) {
+  if (btk_validate(m, n, k, b, kb) != BTK_OK || !dtype_ok(dtype)) return 0;
+  Problem p{};
+  p.x = reinterpret_cast<const void*>(uintptr_t(256));
+  p.row_stride = row_stride;
+  p.dtype = dtype;
+  p.m = m; p.n = n; p.k = k; p.b = b; p.kb = kb;
+  p.layout = layout;
+  p.geo = geo_for(dtype, n);
+  return fused_supported(p) ? 1 : 0;
+}
+
+int btk_launch_count(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, int dtype,
+                     int layout, int64_t row_stride) {
+  if (btk_validate(m, n, k, b, kb) != BTK_OK || !dtype_ok(dtype)) return 0;
+  if (btk_uses_fused_path(m, n, k, b, kb, dtype, layout, row_stride)) return 1;
+  auto k2n = [](int64_t L, int64_t kk) { return L <= K2_SMALL_CAP ? 1 : 2; };
+  if (b == 1) return 1 + k2n(n, k);
+  int c = (kb <= 16) ? 1 : 1 + k2n(ceil_div(n, b), kb);
+  return c + k2n(b * kb, k);
+}
+
+int btk_approx_topk(const void* x, int64_t row_stride, int dtype, int64_t m, int64_t n, int64_t k,
+                    int64_t b, int64_t kb, int layout, void* out_vals, int64_t* out_idx, void* ws,
+                    size_t ws_bytes, uint32_t* flag, void* stream) {
+  int rc = btk_validate(m, n, k, b, kb);
+  if (rc) return rc;
+  rc = check_common(x, dtype, layout, n, row_stride);
+  if (rc) return rc;
+  if (!out_vals || !out_idx) return BTK_ERR_SHAPE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Problem p{};
+  p.x = x;
+  p.row_stride = row_stride;
+  p.dtype = dtype;
+  p.m = m; p.n = n; p.k = k; p.b = b; p.kb = kb;
+  p.layout = layout;
+  p.geo = geo_for(dtype, n);
+  p.flag = flag;
+  if (fused_supported(p)) return cuda_status(run_fused(p, out_vals, out_idx, st));
+
+  const Plan pl = plan_generic(m, n, k, b, kb);
+  if (ws_bytes < pl.total() || (pl.total() && (reinterpret_cast<uintptr_t>(ws) & 255)))
+    return BTK_ERR_WORKSPACE;
+  Carve cv{static_cast<uint8_t*>(ws)};
+  if (b == 1) {
+    // single bucket: Stage 1 is already the exact canonical top-k (k_b == k)
+    uint64_t* mat = cv.take(pl.mat);
+    cv.take(pl.pool);
+    uint64_t* s2a = cv.take(pl.s2a);
+    uint64_t* s2b = cv.take(pl.s2b);
+    rc = cuda_status(run_materialize(p, mat, st));
+    if (rc) return rc;
+    K2Args a{};
+    a.in = mat; a.in_stride = n; a.nseg = m; a.L = n; a.kk = k;
+    a.out_vals = out_vals; a.out_idx = out_idx; a.out_stride = k;
+    a.geo = p.geo; a.scratch_a = s2a; a.scratch_b = s2b;
+    return cuda_status(run_k2(dtype, true, a, st));
+  }
+  uint64_t* pool = cv.take(pl.pool);
+  Carve cv1 = cv;  // stage-1 scratch (mat, s1a, s1b) is dead before stage 2
+  rc = stage1_pool(p, pl, cv1, pool, st);
+  if (rc) return rc;
+  cv.take(pl.mat); cv.take(pl.s1a); cv.take(pl.s1b);
+  uint64_t* s2a = cv.take(pl.s2a);
+  uint64_t* s2b = cv.take(pl.s2b);
+  K2Args a{};
+  a.in = pool; a.in_stride = b * kb; a.nseg = m; a.L = b * kb; a.kk = k;
+  a.out_vals = out_vals; a.out_idx = out_idx; a.out_stride = k;
+  a.geo = p.geo; a.scratch_a = s2a; a.scratch_b = s2b;
+  return cuda_status(run_k2(dtype, true, a, st));
+}
+
+size_t btk_stage1_workspace_bytes(int64_t m, int64_t n, int64_t b, int64_t kb, int dtype,
+                                  int layout) {
+  (void)dtype;
+  (void)layout;
+  if (btk_stage1_validate(n, b, kb) != BTK_OK || m < 1) return 0;
+  Plan pl = plan_generic(m, n, std::max<int64_t>(1, std::min<int64_t>(n, b * kb)), b, kb);
+  pl.pool = (size_t)(m * b * kb * 8);
+  pl.s2a = pl.s2b = 0;
+  if (b == 1) {  // stage1 for b == 1 runs the bucket path too
+    pl.mat = (size_t)(m * n * 8);
+    pl.s1a = pl.s1b = (n > K2_SMALL_CAP && kb > 16) ? (size_t)(m * kb * 8) : 0;
+  }
+  return pl.total();
+}
+
+int btk_stage1(const void* x, int64_t row_stride, int dtype, int64_t m, int64_t n, int64_t b,
+               int64_t kb, int layout, void* out_vals, int64_t* out_idx, void* ws,
+               size_t ws_bytes, uint32_t* flag, void* stream) {
+  if (m < 1) return BTK_ERR_SHAPE;
+  int rc = btk_stage1_validate(n, b, kb);
+  if (rc) return rc;
+  rc = check_common(x, dtype, layout, n, row_stride);
+  if (rc) return rc;
+  const size_t need = btk_stage1_workspace_bytes(m, n, b, kb, dtype, layout);
+  if (ws_bytes < need || (need && (reinterpret_cast<uintptr_t>(ws) & 255))) return BTK_ERR_WORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Problem p{};
+  p.x = x; p.row_stride = row_stride; p.dtype = dtype;
+  p.m = m; p.n = n; p.k = std::min<int64_t>(n, b * kb); p.b = b; p.kb = kb;
+  p.layout = layout; p.geo = geo_for(dtype, n); p.flag = flag;
+  Plan pl = plan_generic(m, n, p.k, b, kb);
+  pl.pool = (size_t)(m * b * kb * 8);
+  if (b == 1) {
+    pl.mat = (size_t)(m * n * 8);
+    pl.s1a = pl.s1b = (n > K2_SMALL_CAP && kb > 16) ? (size_t)(m * kb * 8) : 0;
+  }
+  Carve cv{static_cast<uint8_t*>(ws)};
+  uint64_t* pool = cv.take(pl.pool);
+  rc = stage1_pool(p, pl, cv, pool, st);
+  if (rc) return rc;
+  const int64_t C = btk_stage1_count(n, b, kb, layout);
+  return cuda_status(run_stage1_emit(p, pool, C, out_vals, out_idx, st));
+}
+
+size_t btk_exact_workspace_bytes(int64_t m, int64_t n, int64_t k, int dtype) {
+  return btk_workspace_bytes(m, n, k, 1, k, dtype, BTK_INTERLEAVED);
+}
+
+int btk_exact_topk(const void* x, int64_t row_stride, int dtype, int64_t m, int64_t n, int64_t k,
+                   void* out_vals, int64_t* out_idx, void* ws, size_t ws_bytes, uint32_t* flag,
+                   void* stream) {
+  return btk_approx_topk(x, row_stride, dtype, m, n, k, 1, k, BTK_INTERLEAVED, out_vals, out_idx,
+                         ws, ws_bytes, flag, stream);
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// topk_with_indices: comps from (value, carried label)
+namespace {
+template <int DT>
+__global__ void label_comps(const void* __restrict__ vals, const int64_t* __restrict__ labels,
+                            int64_t total, uint64_t* __restrict__ out, CompGeo g, uint32_t* flag) {
+  bool bad = false, badlab = false;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t bits = load_bits<DT>(vals, t);
+    const int64_t lab = labels[t];
+    bad |= nonfinite<DT>(bits);
+    badlab |= (lab < 0) || (lab > (int64_t)g.imax);
+    out[t] = make_comp(vkey<DT>(bits), (uint32_t)lab, is_negzero<DT>(bits), g);
+  }
+  const int b1 = __syncthreads_or(bad), b2 = __syncthreads_or(badlab);
+  if (threadIdx.x == 0 && flag && (b1 || b2)) atomicOr(flag, (b1 ? 1u : 0u) | (b2 ? 2u : 0u));
+}
+}  // namespace
+
+extern "C" {
+
+size_t btk_topk_with_indices_workspace_bytes(int64_t m, int64_t c, int64_t k, int dtype) {
+  (void)dtype;
+  if (m < 1 || c < 1 || k < 1 || k > c) return 0;
+  size_t v = al((size_t)(m * c * 8));
+  if (c > K2_SMALL_CAP) v += 2 * al((size_t)(m * k * 8));
+  return v;
+}
+
+int btk_topk_with_indices(const void* values, const int64_t* labels, int dtype, int64_t m,
+                          int64_t c, int64_t k, void* out_vals, int64_t* out_idx, void* ws,
+                          size_t ws_bytes, uint32_t* flag, void* stream) {
+  if (!dtype_ok(dtype)) return BTK_ERR_DTYPE;
+  if (m < 1 || c < 1) return BTK_ERR_SHAPE;
+  if (k < 1) return BTK_ERR_NONPOSITIVE;
+  if (k > c) return BTK_ERR_K_GT_N;
+  const size_t need = btk_topk_with_indices_workspace_bytes(m, c, k, dtype);
+  if (ws_bytes < need || (reinterpret_cast<uintptr_t>(ws) & 255)) return BTK_ERR_WORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const CompGeo g = geo_for(dtype, int64_t(1) << 31);
+  Carve cv{static_cast<uint8_t*>(ws)};
+  uint64_t* comps = cv.take((size_t)(m * c * 8));
+  uint64_t* sa = c > K2_SMALL_CAP ? cv.take((size_t)(m * k * 8)) : nullptr;
+  uint64_t* sb = c > K2_SMALL_CAP ? cv.take((size_t)(m * k * 8)) : nullptr;
+  const int64_t total = m * c;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 64));
+  switch (dtype) {
+    case BTK_F32: label_comps<F32><<<grid, 256, 0, st>>>(values, labels, total, comps, g, flag); break;
+    case BTK_BF16: label_comps<BF16><<<grid, 256, 0, st>>>(values, labels, total, comps, g, flag); break;
+    default: label_comps<F16><<<grid, 256, 0, st>>>(values, labels, total, comps, g, flag); break;
+  }
+  int rc = cuda_status(cudaGetLastError());
+  if (rc) return rc;
+  K2Args a{};
+  a.in = comps; a.in_stride = c; a.nseg = m; a.L = c; a.kk = k;
+  a.out_vals = out_vals; a.out_idx = out_idx; a.out_stride = k;
+  a.geo = g; a.scratch_a = sa; a.scratch_b = sb;
+  return cuda_status(run_k2(dtype, true, a, st));
+}
+
+int64_t btk_min_bytes(int64_t m, int64_t n, int64_t k, int64_t vb, int64_t ib) {
+  return m * (n * vb + k * (vb + ib));
+}
+
+const char* btk_error_code(int s) {
+  switch (s) {
+    case BTK_OK: return "";
+    case BTK_ERR_NONPOSITIVE: return "nonpositive";
+    case BTK_ERR_K_GT_N: return "k_gt_n";
+    case BTK_ERR_B_GT_N: return "b_gt_n";
+    case BTK_ERR_KB_RANGE: return "kb_range";
+    case BTK_ERR_UNDERSAMPLED: return "undersampled";
+    case BTK_ERR_INSUFFICIENT_CANDIDATES: return "insufficient_candidates";
+    case BTK_ERR_CHUNKS_RANGE: return "chunks_range";
+    case BTK_ERR_ASSIGNMENT: return "assignment";
+    case BTK_ERR_DTYPE: return "dtype";
+    case BTK_ERR_SHAPE: return "shape";
+    case BTK_ERR_WORKSPACE: return "workspace";
+    case BTK_ERR_ALIGNMENT: return "alignment";
+    case BTK_ERR_CUDA: return "cuda";
+    case BTK_ERR_LABEL_RANGE: return "label_range";
+  }
+  return "unknown";
+}
+
+const char* btk_error_string(int s) {
+  switch (s) {
+    case BTK_OK: return "ok";
+    case BTK_ERR_NONPOSITIVE: return "all of m, n, k, b, k_b must be positive integers";
+    case BTK_ERR_K_GT_N: return "k > n";
+    case BTK_ERR_B_GT_N: return "b > n";
+    case BTK_ERR_KB_RANGE: return "k_b out of range 1..min(k, ceil(n/b))";
+    case BTK_ERR_UNDERSAMPLED: return "b*kb < k";
+    case BTK_ERR_INSUFFICIENT_CANDIDATES: return "stage 1 yields fewer than k candidates";
+    case BTK_ERR_CHUNKS_RANGE: return "chunks_per_bucket must be >= 2";
+    case BTK_ERR_ASSIGNMENT: return "unknown assignment";
+    case BTK_ERR_DTYPE: return "unsupported dtype (float32, bfloat16, float16)";
+    case BTK_ERR_SHAPE: return "scores must be a non-empty m x n matrix";
+    case BTK_ERR_WORKSPACE: return "workspace too small or not 256-byte aligned";
+    case BTK_ERR_ALIGNMENT: return "misaligned device pointer";
+    case BTK_ERR_CUDA: return "CUDA launch failed";
+    case BTK_ERR_LABEL_RANGE: return "carried label outside [0, 2^31-1]";
+  }
+  return "unknown status";
+}
+
+int btk_last_cuda_error(void) { return g_last_cuda; }
+
+const char* btk_version(void) { return "btk 0.1 sm_100a"; }
+
+}  // extern "C"

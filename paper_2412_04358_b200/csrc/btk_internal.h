@@ -1,0 +1,76 @@
+// Internal (non-ABI) declarations shared by the library's translation units.
+#pragma once
+
+#include <algorithm>
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "btk_common.cuh"
+
+namespace btk {
+
+// Longest segment K2 sorts entirely in one CTA's shared memory.
+constexpr int64_t K2_SMALL_CAP = 16384;
+
+struct K2Args {
+  const uint64_t* in;   // nseg segments of L keys (row stride in_stride)
+  int64_t in_stride;
+  int64_t nseg;
+  int64_t L;
+  int64_t kk;           // keep the kk largest, sorted descending
+  uint64_t* out_keys;   // !decode: nseg x kk comps (row stride out_stride)
+  void* out_vals;       // decode: values (input dtype) ...
+  int64_t* out_idx;     //         ... and int64 indices
+  int64_t out_stride;
+  CompGeo geo;
+  uint64_t* scratch_a;  // long segments only: nseg * kk keys each
+  uint64_t* scratch_b;
+};
+
+// Opt a kernel into >48 KB dynamic smem once per device (never during
+// stream capture, where the warm-up call has already done it).
+inline cudaError_t ensure_smem_attr(const void* fn, size_t bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  static thread_local const void* done_fn[64];
+  static thread_local int done_dev[64];
+  static thread_local int n_done = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  for (int i = 0; i < n_done; ++i)
+    if (done_fn[i] == fn && done_dev[i] == dev) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess && n_done < 64) { done_fn[n_done] = fn; done_dev[n_done] = dev; ++n_done; }
+  return e;
+}
+
+cudaError_t run_k2(int dtype, bool decode, const K2Args& a, cudaStream_t st);
+cudaError_t run_decode(int dtype, const uint64_t* in, int64_t in_stride, int64_t nseg, int64_t kk,
+                       void* out_vals, int64_t* out_idx, int64_t out_stride, CompGeo g,
+                       cudaStream_t st);
+
+// Problem description shared by the stage-1 launchers.
+struct Problem {
+  const void* x;
+  int64_t row_stride;  // elements
+  int dtype;
+  int64_t m, n, k, b, kb;
+  int layout;          // 0 interleaved, 1 contiguous
+  CompGeo geo;
+  uint32_t* flag;      // device non-finite flag (may be null)
+};
+
+// Generic stage 1, k_b <= 16: one thread per (row, bucket), register queue.
+// pool: m x (b*kb) comps, bucket-major, sorted within bucket, 0 = empty.
+cudaError_t run_stage1_generic(const Problem& p, uint64_t* pool, cudaStream_t st);
+// All of a row's elements as comps, bucket-major (m*b segments of s slots).
+cudaError_t run_materialize(const Problem& p, uint64_t* mat, cudaStream_t st);
+// pool (m x b*kb) -> compact (m x C) values/indices in bucket order.
+cudaError_t run_stage1_emit(const Problem& p, const uint64_t* pool, int64_t C, void* out_vals,
+                            int64_t* out_idx, cudaStream_t st);
+// Fused interleaved fast path (stage 1 + stage 2 in one kernel per row group).
+// Returns cudaErrorNotSupported when the shape is outside its envelope.
+cudaError_t run_fused(const Problem& p, void* out_vals, int64_t* out_idx, cudaStream_t st);
+bool fused_supported(const Problem& p);
+
+}  // namespace btk

@@ -1,0 +1,280 @@
+// K2: segmented exact top-kk over composite keys, emitted in canonical order.
+//
+// Restates reference exact.py:142-159 (topk_with_indices / _canonical_order)
+// for the GPU: candidates of one segment (a row's Stage-1 survivors, or one
+// bucket when k_b is large) are reduced to their kk largest composite keys,
+// sorted descending.  Because comps are unique and their unsigned order is
+// (value desc, index asc), "sort comps descending, take kk" IS the
+// reference's two stable argsorts.
+//
+//   L <= SMALL_CAP : one CTA per segment, keys resident in shared memory,
+//                    LSD radix sort (btk_sort.cuh), epilogue writes kk.
+//   L >  SMALL_CAP : k2_select_compact (MSD radix select of the kk-th key
+//                    with 256-bin smem histograms, then compaction), then
+//                    the smem sort if kk fits, else k2_global_lsd (stable
+//                    LSD passes through a global ping-pong buffer).
+#include "btk_internal.h"
+#include "btk_sort.cuh"
+
+namespace btk {
+
+template <int DT>
+__device__ __forceinline__ void emit(uint64_t c, int64_t pos, const CompGeo& g, void* out_vals,
+                                     int64_t* out_idx) {
+  uint32_t bits;
+  int64_t idx;
+  decode_comp<DT>(c, g, bits, idx);
+  store_bits<DT>(out_vals, pos, bits);
+  out_idx[pos] = idx;
+}
+
+// ---------------------------------------------------------------------------
+template <int DT, int NT, int ITEMS, bool DECODE>
+__global__ void __launch_bounds__(NT) k2_small(const uint64_t* __restrict__ in, int64_t in_stride,
+                                               int64_t L, int64_t kk, uint64_t* __restrict__ out_keys,
+                                               void* __restrict__ out_vals,
+                                               int64_t* __restrict__ out_idx, int64_t out_stride,
+                                               CompGeo g) {
+  constexpr int N = NT * ITEMS;
+  constexpr int NW = NT / 32;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw);
+  uint32_t* whist = reinterpret_cast<uint32_t*>(sk + N);
+  uint32_t* dbase = whist + NW * RADIX;
+  uint32_t* dtotal = dbase + RADIX;
+  const int64_t seg = blockIdx.x;
+  const uint64_t* src = in + seg * in_stride;
+  for (int p = threadIdx.x; p < N; p += NT) sk[p] = (p < L) ? src[p] : 0ull;
+  __syncthreads();
+  // bit 0 (negzero) never decides the order of unique comps
+  block_sort_desc<NT, ITEMS>(sk, whist, dbase, dtotal, 1, g.nbits);
+  for (int p = threadIdx.x; p < kk; p += NT) {
+    if constexpr (DECODE) {
+      emit<DT>(sk[p], seg * out_stride + p, g, out_vals, out_idx);
+    } else {
+      out_keys[seg * out_stride + p] = sk[p];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// MSD radix select + compaction for one long segment per CTA.
+template <int NT>
+__global__ void __launch_bounds__(NT) k2_select_compact(const uint64_t* __restrict__ in,
+                                                        int64_t in_stride, int64_t L, int64_t kk,
+                                                        uint64_t* __restrict__ out,
+                                                        int64_t out_stride, int nbits) {
+  __shared__ uint32_t hist[RADIX];
+  __shared__ int s_bin;
+  __shared__ uint32_t s_above;
+  __shared__ uint32_t s_cnt;
+  const int64_t seg = blockIdx.x;
+  const uint64_t* src = in + seg * in_stride;
+  uint64_t* dst = out + seg * out_stride;
+  uint64_t prefix = 0;
+  uint32_t need = (uint32_t)kk;
+  int shift = nbits;
+  bool early = false;
+  while (shift > 0) {
+    const int w = (shift % 8) ? (shift % 8) : 8;
+    shift -= w;
+    for (int j = threadIdx.x; j < RADIX; j += NT) hist[j] = 0;
+    __syncthreads();
+    const int hs = shift + w;
+    for (int64_t p = threadIdx.x; p < L; p += NT) {
+      uint64_t key = src[p];
+      uint64_t hi = (hs >= 64) ? 0ull : (key >> hs);
+      if (hi == prefix) atomicAdd(&hist[(uint32_t)(key >> shift) & ((1u << w) - 1u)], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) find_crossing_desc(hist, need, &s_bin, &s_above);
+    __syncthreads();
+    const int bin = s_bin;
+    need -= s_above;
+    prefix = (prefix << w) | (uint64_t)bin;
+    const uint32_t inbin = hist[bin];
+    __syncthreads();
+    if (inbin == need) { early = true; break; }
+  }
+  // early: selected = {key >= prefix << shift}, exactly kk of them.
+  // else : thr = prefix is an exact key value; {key > thr} has kk - need
+  //        members, remaining slots are copies of thr (only the empty
+  //        sentinel 0 can repeat).
+  const uint64_t thr = early ? (prefix << shift) : prefix;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (int64_t p0 = 0; p0 < L; p0 += NT) {
+    int64_t p = p0 + threadIdx.x;
+    uint64_t key = (p < L) ? src[p] : 0ull;
+    bool take = (p < L) && (early ? (key >= thr) : (key > thr));
+    uint32_t ball = __ballot_sync(0xFFFFFFFFu, take);
+    uint32_t base = 0;
+    if (lane == 0 && ball) base = atomicAdd(&s_cnt, (uint32_t)__popc(ball));
+    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    if (take) dst[base + __popc(ball & lanemask_lt())] = key;
+  }
+  __syncthreads();
+  for (int64_t p = s_cnt + threadIdx.x; p < kk; p += NT) dst[p] = thr;
+}
+
+// ---------------------------------------------------------------------------
+// Stable LSD sort of kk keys per segment through a global ping-pong buffer,
+// one CTA per segment; the epilogue writes the sorted keys out.
+template <int DT, int NT, int ITEMS, bool DECODE>
+__global__ void __launch_bounds__(NT) k2_global_lsd(uint64_t* __restrict__ A, uint64_t* __restrict__ B,
+                                                    int64_t stride, int64_t kk,
+                                                    uint64_t* __restrict__ out_keys,
+                                                    void* __restrict__ out_vals,
+                                                    int64_t* __restrict__ out_idx,
+                                                    int64_t out_stride, CompGeo g) {
+  constexpr int N = NT * ITEMS;
+  constexpr int NW = NT / 32;
+  __shared__ uint32_t whist[NW * RADIX];
+  __shared__ uint32_t dtotal[RADIX];
+  __shared__ uint32_t runbase[RADIX];
+  __shared__ uint32_t ghist[RADIX];
+  __shared__ int s_skip;
+  const int64_t seg = blockIdx.x;
+  uint64_t* src = A + seg * stride;
+  uint64_t* dst = B + seg * stride;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int shift = 1; shift < g.nbits; shift += 8) {
+    for (int j = threadIdx.x; j < RADIX; j += NT) ghist[j] = 0;
+    if (threadIdx.x == 0) s_skip = 0;
+    __syncthreads();
+    for (int64_t p = threadIdx.x; p < kk; p += NT) atomicAdd(&ghist[desc_digit(src[p], shift)], 1u);
+    __syncthreads();
+    if (threadIdx.x < RADIX && ghist[threadIdx.x] == (uint32_t)kk) s_skip = 1;
+    if (warp == 0) warp_exscan256(ghist, runbase);
+    __syncthreads();
+    if (s_skip) continue;
+    for (int64_t t0 = 0; t0 < kk; t0 += N) {
+      uint64_t key[ITEMS];
+      uint32_t rank[ITEMS];
+      bool valid[ITEMS];
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        int64_t p = t0 + warp * 32 * ITEMS + i * 32 + lane;
+        valid[i] = p < kk;
+        key[i] = valid[i] ? src[p] : 0ull;  // invalid tail ranks last (digit 255)
+      }
+      uint32_t* wh = whist + warp * RADIX;
+      for (int j = lane; j < RADIX; j += 32) wh[j] = 0;
+      __syncwarp();
+      warp_rank<ITEMS>(key, shift, wh, rank);
+      __syncthreads();
+      warp_offsets<NT>(whist, dtotal);
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        if (valid[i]) {
+          uint32_t d = desc_digit(key[i], shift);
+          dst[runbase[d] + whist[warp * RADIX + d] + rank[i]] = key[i];
+        }
+      }
+      __syncthreads();
+      for (int j = threadIdx.x; j < RADIX; j += NT) runbase[j] += dtotal[j];
+      __syncthreads();
+    }
+    uint64_t* t = src; src = dst; dst = t;
+  }
+  __syncthreads();
+  for (int64_t p = threadIdx.x; p < kk; p += NT) {
+    if constexpr (DECODE) {
+      emit<DT>(src[p], seg * out_stride + p, g, out_vals, out_idx);
+    } else {
+      out_keys[seg * out_stride + p] = src[p];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+template <int DT>
+__global__ void k2_decode(const uint64_t* __restrict__ in, int64_t in_stride, int64_t nseg,
+                          int64_t kk, void* __restrict__ out_vals, int64_t* __restrict__ out_idx,
+                          int64_t out_stride, CompGeo g) {
+  const int64_t total = nseg * kk;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t seg = t / kk, p = t - seg * kk;
+    emit<DT>(in[seg * in_stride + p], seg * out_stride + p, g, out_vals, out_idx);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host dispatch.
+template <int NT, int ITEMS>
+static constexpr size_t small_smem() {
+  return (size_t)NT * ITEMS * 8 + (size_t)(NT / 32) * RADIX * 4 + 2 * RADIX * 4;
+}
+
+template <int DT, int NT, int ITEMS, bool DECODE>
+static cudaError_t launch_small(const K2Args& a, cudaStream_t st) {
+  auto kern = k2_small<DT, NT, ITEMS, DECODE>;
+  constexpr size_t sm = small_smem<NT, ITEMS>();
+  cudaError_t e = ensure_smem_attr((const void*)kern, sm);
+  if (e != cudaSuccess) return e;
+  if (a.nseg == 0) return cudaSuccess;
+  kern<<<(unsigned)a.nseg, NT, sm, st>>>(a.in, a.in_stride, a.L, a.kk, a.out_keys, a.out_vals,
+                                         a.out_idx, a.out_stride, a.geo);
+  return cudaGetLastError();
+}
+
+template <int DT, bool DECODE>
+static cudaError_t run_small(const K2Args& a, cudaStream_t st) {
+  const int64_t L = a.L;
+  if (L <= 256) return launch_small<DT, 64, 4, DECODE>(a, st);
+  if (L <= 1024) return launch_small<DT, 128, 8, DECODE>(a, st);
+  if (L <= 2048) return launch_small<DT, 256, 8, DECODE>(a, st);
+  if (L <= 4096) return launch_small<DT, 512, 8, DECODE>(a, st);
+  if (L <= 8192) return launch_small<DT, 1024, 8, DECODE>(a, st);
+  return launch_small<DT, 1024, 16, DECODE>(a, st);
+}
+
+template <int DT, bool DECODE>
+static cudaError_t run_k2_t(const K2Args& a, cudaStream_t st) {
+  if (a.L <= K2_SMALL_CAP) return run_small<DT, DECODE>(a, st);
+  // long segments
+  if (a.scratch_a == nullptr || a.scratch_b == nullptr) return cudaErrorInvalidValue;
+  k2_select_compact<1024><<<(unsigned)a.nseg, 1024, 0, st>>>(a.in, a.in_stride, a.L, a.kk,
+                                                             a.scratch_a, a.kk, a.geo.nbits);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if (a.kk <= K2_SMALL_CAP) {
+    K2Args b = a;
+    b.in = a.scratch_a;
+    b.in_stride = a.kk;
+    b.L = a.kk;
+    return run_small<DT, DECODE>(b, st);
+  }
+  k2_global_lsd<DT, 512, 8, DECODE><<<(unsigned)a.nseg, 512, 0, st>>>(
+      a.scratch_a, a.scratch_b, a.kk, a.kk, a.out_keys, a.out_vals, a.out_idx, a.out_stride, a.geo);
+  return cudaGetLastError();
+}
+
+cudaError_t run_k2(int dtype, bool decode, const K2Args& a, cudaStream_t st) {
+  switch (dtype) {
+    case F32: return decode ? run_k2_t<F32, true>(a, st) : run_k2_t<F32, false>(a, st);
+    case BF16: return decode ? run_k2_t<BF16, true>(a, st) : run_k2_t<BF16, false>(a, st);
+    case F16: return decode ? run_k2_t<F16, true>(a, st) : run_k2_t<F16, false>(a, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t run_decode(int dtype, const uint64_t* in, int64_t in_stride, int64_t nseg, int64_t kk,
+                       void* out_vals, int64_t* out_idx, int64_t out_stride, CompGeo g,
+                       cudaStream_t st) {
+  int64_t total = nseg * kk;
+  if (total == 0) return cudaSuccess;
+  unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 32);
+  switch (dtype) {
+    case F32: k2_decode<F32><<<grid, 256, 0, st>>>(in, in_stride, nseg, kk, out_vals, out_idx, out_stride, g); break;
+    case BF16: k2_decode<BF16><<<grid, 256, 0, st>>>(in, in_stride, nseg, kk, out_vals, out_idx, out_stride, g); break;
+    case F16: k2_decode<F16><<<grid, 256, 0, st>>>(in, in_stride, nseg, kk, out_vals, out_idx, out_stride, g); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace btk

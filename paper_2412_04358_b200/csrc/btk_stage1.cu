@@ -1,0 +1,173 @@
+// Generic Stage 1: per-bucket top-k_b for any layout / raggedness / dtype.
+//
+// Restates reference approx.py:112-173 + 208-242 (index map, cube gather,
+// top-k_b per bucket, ragged keep-mask) without materialising the cube:
+// one thread owns one (row, bucket), walks the bucket's positions in
+// increasing index order and keeps a register-resident insertion queue of
+// composite keys.  A strict ">" test suffices (the scan order makes any
+// later tie lose), mirroring the reference's "first maximum" argmax.
+//
+// This is the universal path (contiguous layout, ragged shapes, odd
+// strides).  Interleaved shapes inside the fused envelope take
+// btk_fused.cu instead.
+#include "btk_internal.h"
+
+namespace btk {
+
+__device__ __forceinline__ void bucket_span(const Problem& p, int64_t j, int64_t& start,
+                                            int64_t& size, int64_t& step) {
+  if (p.layout == 0) {
+    const int64_t q = p.n / p.b, r = p.n % p.b;
+    start = j;
+    size = q + (j < r ? 1 : 0);
+    step = p.b;
+  } else {
+    start = (j * p.n + p.b - 1) / p.b;
+    const int64_t end = ((j + 1) * p.n + p.b - 1) / p.b;
+    size = end - start;
+    step = 1;
+  }
+}
+
+template <int DT>
+__device__ __forceinline__ uint64_t elem_comp(const Problem& p, const void* row, int64_t idx,
+                                              bool& bad) {
+  const uint32_t bits = load_bits<DT>(row, idx);
+  bad |= nonfinite<DT>(bits);
+  return make_comp(vkey<DT>(bits), (uint32_t)idx, is_negzero<DT>(bits), p.geo);
+}
+
+template <int DT, int KB>
+__global__ void __launch_bounds__(256) s1_generic(Problem p, uint64_t* __restrict__ pool) {
+  const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const int64_t P = p.b * p.kb;
+  bool bad = false;
+  for (int64_t row = blockIdx.y; row < p.m; row += gridDim.y) {
+    if (j < p.b) {
+      const void* xr = static_cast<const uint8_t*>(p.x) +
+                       row * p.row_stride * (VT<DT>::W / 8);
+      int64_t start, size, step;
+      bucket_span(p, j, start, size, step);
+      uint64_t q[KB];
+#pragma unroll
+      for (int i = 0; i < KB; ++i) q[i] = 0ull;
+      for (int64_t t = 0; t < size; ++t) {
+        const uint64_t c = elem_comp<DT>(p, xr, start + t * step, bad);
+        if (c > q[KB - 1]) {
+#pragma unroll
+          for (int i = KB - 1; i > 0; --i) q[i] = (c > q[i - 1]) ? q[i - 1] : (c > q[i] ? c : q[i]);
+          q[0] = (c > q[0]) ? c : q[0];
+        }
+      }
+      uint64_t* dst = pool + row * P + j * p.kb;
+#pragma unroll
+      for (int i = 0; i < KB; ++i)
+        if (i < p.kb) dst[i] = q[i];
+    }
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0 && p.flag) atomicOr(p.flag, 1u);
+}
+
+template <int DT>
+__global__ void s1_materialize(Problem p, uint64_t* __restrict__ mat) {
+  const int64_t s = (p.n + p.b - 1) / p.b;
+  const int64_t total = p.m * p.b * s;
+  bool bad = false;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t slot = t % s;
+    const int64_t rb = t / s;
+    const int64_t j = rb % p.b, row = rb / p.b;
+    int64_t start, size, step;
+    bucket_span(p, j, start, size, step);
+    uint64_t c = 0ull;
+    if (slot < size) {
+      const void* xr = static_cast<const uint8_t*>(p.x) + row * p.row_stride * (VT<DT>::W / 8);
+      c = elem_comp<DT>(p, xr, start + slot * step, bad);
+    }
+    mat[t] = c;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0 && p.flag) atomicOr(p.flag, 1u);
+}
+
+template <int DT>
+__global__ void s1_emit(Problem p, const uint64_t* __restrict__ pool, int64_t C,
+                        void* __restrict__ out_vals, int64_t* __restrict__ out_idx) {
+  const int64_t total = p.m * p.b * p.kb;
+  const int64_t q0 = p.n / p.b, r = p.n % p.b;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t qq = t % p.kb;
+    const int64_t rb = t / p.kb;
+    const int64_t j = rb % p.b, row = rb / p.b;
+    int64_t start, size, step;
+    bucket_span(p, j, start, size, step);
+    if (qq >= size) continue;
+    // closed-form bucket offset of sum_{j'<j} min(kb, size_j') (core.py:155-158)
+    int64_t off;
+    if (p.kb <= q0) off = j * p.kb;
+    else off = (p.layout == 0) ? (j * q0 + (j < r ? j : r)) : start;
+    uint32_t bits;
+    int64_t idx;
+    decode_comp<DT>(pool[t], p.geo, bits, idx);
+    store_bits<DT>(out_vals, row * C + off + qq, bits);
+    out_idx[row * C + off + qq] = idx;
+  }
+}
+
+// ---------------------------------------------------------------------------
+template <int DT, int KB>
+static cudaError_t launch_generic(const Problem& p, uint64_t* pool, cudaStream_t st) {
+  dim3 grid((unsigned)((p.b + 255) / 256), (unsigned)std::min<int64_t>(p.m, 65535));
+  s1_generic<DT, KB><<<grid, 256, 0, st>>>(p, pool);
+  return cudaGetLastError();
+}
+
+template <int DT>
+static cudaError_t generic_t(const Problem& p, uint64_t* pool, cudaStream_t st) {
+  if (p.kb <= 1) return launch_generic<DT, 1>(p, pool, st);
+  if (p.kb <= 2) return launch_generic<DT, 2>(p, pool, st);
+  if (p.kb <= 4) return launch_generic<DT, 4>(p, pool, st);
+  if (p.kb <= 8) return launch_generic<DT, 8>(p, pool, st);
+  if (p.kb <= 16) return launch_generic<DT, 16>(p, pool, st);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t run_stage1_generic(const Problem& p, uint64_t* pool, cudaStream_t st) {
+  switch (p.dtype) {
+    case F32: return generic_t<F32>(p, pool, st);
+    case BF16: return generic_t<BF16>(p, pool, st);
+    case F16: return generic_t<F16>(p, pool, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+static unsigned grid_for(int64_t total) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 64));
+}
+
+cudaError_t run_materialize(const Problem& p, uint64_t* mat, cudaStream_t st) {
+  const int64_t s = (p.n + p.b - 1) / p.b;
+  const unsigned g = grid_for(p.m * p.b * s);
+  switch (p.dtype) {
+    case F32: s1_materialize<F32><<<g, 256, 0, st>>>(p, mat); break;
+    case BF16: s1_materialize<BF16><<<g, 256, 0, st>>>(p, mat); break;
+    case F16: s1_materialize<F16><<<g, 256, 0, st>>>(p, mat); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t run_stage1_emit(const Problem& p, const uint64_t* pool, int64_t C, void* out_vals,
+                            int64_t* out_idx, cudaStream_t st) {
+  const unsigned g = grid_for(p.m * p.b * p.kb);
+  switch (p.dtype) {
+    case F32: s1_emit<F32><<<g, 256, 0, st>>>(p, pool, C, out_vals, out_idx); break;
+    case BF16: s1_emit<BF16><<<g, 256, 0, st>>>(p, pool, C, out_vals, out_idx); break;
+    case F16: s1_emit<F16><<<g, 256, 0, st>>>(p, pool, C, out_vals, out_idx); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace btk

@@ -1,0 +1,236 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle / golden vectors.
+
+Bar: bit-exact indices and value bits (sign of zero included), every case.
+"""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2412_04358_b200 as btk
+from oracle import bucketed_oracle as O
+from tests.golden_io import baseline_cases, load, sha, small_cases
+
+pytestmark = pytest.mark.gpu
+
+I, C = btk.Assignment.INTERLEAVED, btk.Assignment.CONTIGUOUS
+DT = {"f32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16}
+
+
+def _asg(s):
+    return I if s == "interleaved" else C
+
+
+def _bits(t: torch.Tensor) -> np.ndarray:
+    t = t.detach().cpu()
+    if t.dtype == torch.float32:
+        return t.view(torch.int32).numpy()
+    return t.view(torch.int16).numpy()
+
+
+def _want_bits(v64: np.ndarray, dtype) -> np.ndarray:
+    return _bits(torch.from_numpy(np.asarray(v64, np.float64)).to(dtype))
+
+
+def assert_same(res, want_v, want_i, dtype):
+    got_i = res.indices.cpu().numpy()
+    assert got_i.dtype == np.int64
+    np.testing.assert_array_equal(got_i, want_i)
+    np.testing.assert_array_equal(_bits(res.values), _want_bits(want_v, dtype))
+
+
+def _dtypes_for(x32: np.ndarray):
+    out = ["f32"]
+    for name, tdt in (("bf16", torch.bfloat16), ("f16", torch.float16)):
+        t = torch.from_numpy(x32)
+        if torch.equal(t.to(tdt).float(), t) and np.all(np.isfinite(t.to(tdt).float().numpy())):
+            out.append(name)
+    return out
+
+
+SMALL = small_cases()
+
+
+@pytest.mark.parametrize("case", SMALL, ids=[c["name"] for c in SMALL])
+def test_small_golden(case):
+    x32 = np.ascontiguousarray(case["x"], np.float32)
+    for dn in _dtypes_for(x32):
+        x = torch.from_numpy(x32).to(DT[dn]).cuda()
+        sch = btk.BucketScheme(case["b"], case["kb"], _asg(case["asg"]))
+        r = btk.approx_topk(x, case["k"], sch)
+        assert_same(r, case["values"], case["indices"], DT[dn])
+        s1 = btk.stage1(x, sch)
+        np.testing.assert_array_equal(s1.indices.cpu().numpy(), case["s1_indices"])
+        np.testing.assert_array_equal(_bits(s1.values), _want_bits(case["s1_values"], DT[dn]))
+        np.testing.assert_array_equal(s1.per_bucket, case["s1_per_bucket"])
+        e = btk.exact_topk_oracle(x, case["k"])
+        assert_same(e, case["ex_values"], case["ex_indices"], DT[dn])
+
+
+def test_worked_example_literals():
+    row = torch.tensor([11.0, 3.0, 10.0, 6.0, 1.0, 4.0, 8.0, 5.0, 2.0, 9.0, 7.0], device="cuda")
+    sch = btk.BucketScheme(3, 2, I)
+    c = btk.stage1(row, sch)
+    assert c.values[0].tolist() == [11, 9, 7, 5, 10, 4]
+    assert c.indices[0].tolist() == [0, 9, 10, 7, 2, 5]
+    assert c.per_bucket.tolist() == [2, 2, 2]
+    r = btk.approx_topk(row, 4, sch)
+    assert r.values[0].tolist() == [11, 10, 9, 7] and r.indices[0].tolist() == [0, 2, 9, 10]
+    e = btk.exact_topk_oracle(row, 4)
+    assert e.values[0].tolist() == [11, 10, 9, 8] and e.indices[0].tolist() == [0, 2, 9, 6]
+
+
+@pytest.mark.parametrize("case", baseline_cases(), ids=lambda c: c["name"])
+def test_baseline_shapes_golden(case):
+    x32 = case["gen"]()
+    assert sha(x32) == case["sha"]
+    dt = torch.float32
+    if case["kind"] == "normal_bf16":
+        dt = torch.bfloat16
+    elif case["kind"] == "normal_f16":
+        dt = torch.float16
+    x = torch.from_numpy(x32).to(dt).cuda()
+    r = btk.approx_topk(x, case["k"], btk.BucketScheme(case["b"], case["kb"], I))
+    np.testing.assert_array_equal(r.indices.cpu().numpy(), case["indices"])
+    np.testing.assert_array_equal(r.values.float().cpu().numpy(), case["values"])
+
+
+def test_carried_labels():
+    z = load("carried_labels.npz")
+    r = btk.topk_with_indices(torch.tensor(z["v"], dtype=torch.float32), z["lab"], int(z["k"]))
+    assert r.indices[0].tolist() == [10, 30, 20]
+    assert r.values[0].tolist() == [9.0, 9.0, 5.0]
+    r = btk.topk_with_indices(torch.tensor(z["v2"]), z["lab2"], int(z["k2"]))
+    np.testing.assert_array_equal(r.indices.cpu().numpy(), z["indices2"])
+    np.testing.assert_array_equal(r.values.double().cpu().numpy(), z["values2"])
+
+
+def test_nonfinite_raises():
+    for bad in (float("nan"), float("inf"), float("-inf")):
+        for dt in DT.values():
+            x = torch.zeros(3, 64, dtype=dt, device="cuda")
+            x[1, 17] = bad
+            with pytest.raises(btk.NonFiniteInputError):
+                btk.approx_topk(x, 8, btk.BucketScheme(8, 1, I))
+            with pytest.raises(btk.NonFiniteInputError):
+                btk.exact_topk_oracle(x, 4)
+            # opt-out: no raise
+            btk.approx_topk(x, 8, btk.BucketScheme(8, 1, I), check_finite=False)
+
+
+def test_config_errors_match_reference_codes():
+    z = load("validation.npz")
+    x = torch.zeros(64, device="cuda")
+    for p, code in zip(z["params"], z["codes"]):
+        m, n, k, b, kb = (int(v) for v in p)
+        got = ""
+        try:
+            btk.check_parameters(m, n, k, b, kb)
+        except btk.ConfigError as e:
+            got = e.code
+        assert got == str(code)
+    with pytest.raises(btk.ConfigError) as e:
+        btk.approx_topk(torch.arange(8.0, device="cuda"), 4, btk.BucketScheme(2, 1, I))
+    assert e.value.code == "undersampled" and "b*kb < k" in str(e.value)
+    del x
+
+
+def _rand_input(rng, kind, m, n):
+    if kind == "normal":
+        return rng.standard_normal((m, n), dtype=np.float32)
+    if kind == "ties":
+        return rng.integers(-3, 4, size=(m, n)).astype(np.float32)
+    x = rng.integers(-1, 2, size=(m, n)).astype(np.float32) * 0.0  # +-0 soup
+    x[rng.random((m, n)) < 0.2] = 1.0
+    return x
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_sweep_vs_oracle(seed):
+    rng = np.random.default_rng(1000 + seed)
+    for _ in range(25):
+        n = int(rng.integers(1, 5000))
+        b = int(rng.integers(1, n + 1))
+        cap = -(-n // b)
+        kb = int(rng.integers(1, min(cap, 40) + 1))
+        k = int(rng.integers(kb, min(n, b * kb) + 1))
+        asg = "interleaved" if rng.random() < 0.6 else "contiguous"
+        kind = ["normal", "ties", "zeros"][int(rng.integers(3))]
+        m = int(rng.integers(1, 5))
+        x32 = _rand_input(rng, kind, m, n)
+        wv, wi = O.approx_topk(x32, k, b, kb, asg)
+        for dn in _dtypes_for(x32):
+            x = torch.from_numpy(x32).to(DT[dn]).cuda()
+            r = btk.approx_topk(x, k, btk.BucketScheme(b, kb, _asg(asg)))
+            assert_same(r, wv, wi, DT[dn])
+
+
+@pytest.mark.parametrize("n,k,b,kb", [
+    (50000, 20000, 1, 20000),      # exact path, long segment, global LSD sort
+    (40000, 3000, 1, 3000),        # long segment, select then smem sort
+    (70000, 4000, 2, 2000),        # kb > 16 with s > 16384
+    (65536, 18000, 9000, 2),       # pool > 16384 -> select_compact + global lsd
+    (100003, 5000, 40000, 1),      # ragged, pool > cap, kk fits smem
+])
+def test_long_segment_paths(n, k, b, kb):
+    rng = np.random.default_rng(n + k)
+    x32 = rng.standard_normal((2, n), dtype=np.float32)
+    x32[:, ::7] = np.round(x32[:, ::7])  # ties
+    wv, wi = O.approx_topk(x32, k, b, kb, "interleaved")
+    r = btk.approx_topk(torch.from_numpy(x32).cuda(), k, btk.BucketScheme(b, kb, I))
+    assert_same(r, wv, wi, torch.float32)
+
+
+def test_dim_and_strides():
+    rng = np.random.default_rng(3)
+    x32 = rng.standard_normal((5, 300, 4), dtype=np.float32)
+    x = torch.from_numpy(x32).cuda()
+    sch = btk.BucketScheme(30, 2, I)
+    r = btk.approx_topk(x, 40, sch, dim=1)
+    assert tuple(r.values.shape) == (5, 40, 4)
+    flat = np.moveaxis(x32, 1, -1).reshape(-1, 300)
+    wv, wi = O.approx_topk(flat, 40, 30, 2)
+    got_i = r.indices.movedim(1, -1).reshape(-1, 40).cpu().numpy()
+    np.testing.assert_array_equal(got_i, wi)
+    # a non-contiguous row view
+    big = torch.from_numpy(rng.standard_normal((4, 1000), dtype=np.float32)).cuda()
+    view = big[:, 100:900]
+    wv, wi = O.approx_topk(view.cpu().numpy(), 32, 32, 1)
+    r = btk.approx_topk(view, 32, btk.BucketScheme(32, 1, I))
+    np.testing.assert_array_equal(r.indices.cpu().numpy(), wi)
+
+
+def test_full_config1_and_determinism():
+    rng = np.random.default_rng(7)
+    x32 = rng.standard_normal((128, 65536), dtype=np.float32)
+    wv, wi = O.approx_topk(x32, 64, 64, 1, workers=os.cpu_count() or 1)
+    x = torch.from_numpy(x32).cuda()
+    sch = btk.BucketScheme(64, 1, I)
+    r1 = btk.approx_topk(x, 64, sch)
+    assert_same(r1, wv, wi, torch.float32)
+    op = btk.ApproxTopK(128, 65536, 64, sch, dtype=torch.float32, device="cuda")
+    for _ in range(3):
+        r = op(x)
+        torch.cuda.synchronize()
+        assert torch.equal(r.indices, r1.indices) and torch.equal(r.values, r1.values)
+
+
+def test_full_config4():
+    rng = np.random.default_rng(8)
+    x32 = rng.standard_normal((4096, 32768), dtype=np.float32)
+    xb = torch.from_numpy(x32).to(torch.bfloat16)
+    wv, wi = O.approx_topk(xb.float().numpy(), 512, 512, 1, workers=os.cpu_count() or 1)
+    r = btk.approx_topk(xb.cuda(), 512, btk.BucketScheme(512, 1, I))
+    assert_same(r, wv, wi, torch.bfloat16)
+
+
+def test_sharded_equals_single():
+    rng = np.random.default_rng(9)
+    x = torch.from_numpy(rng.standard_normal((23, 4096), dtype=np.float32)).cuda()
+    sch = btk.BucketScheme(256, 2, I)
+    base = btk.approx_topk(x, 256, sch)
+    devs = ["cuda:0"] * 3  # same device three times: exercises the partition logic
+    r = btk.approx_topk_sharded(x, 256, sch, devices=devs)
+    assert torch.equal(r.indices, base.indices) and torch.equal(r.values, base.values)
