@@ -1,7 +1,821 @@
-// Fused interleaved fast path (placeholder until the kernel lands).
+// Fused interleaved fast path: Stage 1 + Stage 2 + canonical write, one
+// launch, no HBM round trip for the candidates.
+//
+// Interleaved buckets are the COLUMNS of a row viewed as an (s, b) row-major
+// matrix (reference approx.py:112-131: grid[j, t] = j + b*t), so the
+// reference's strided "gather cube" (approx.py:134-139) is free here: a
+// contiguous run of view-rows is a dense tile whose columns are buckets.
+//
+// Two kernels:
+//
+//  fused_narrow  (b < V*NT: many view-rows per bucket; cfg1, cfg3, cfg4)
+//      A cluster of S CTAs owns one row; CTA c streams view-rows
+//      [c*s/S, (c+1)*s/S) through a shared-memory ring filled by
+//      cp.async.bulk (TMA bulk copies, mbarrier complete_tx), one elected
+//      thread issuing, every thread consuming.  Thread (r, g) owns the V
+//      buckets of vector column g and every R-th view-row of a stage; it
+//      keeps a register queue of the top-KB (value, slot) per bucket.
+//      The R phase-queues are merged in smem, the S CTA partials are merged
+//      by the leader through DSMEM, then the leader sorts the b*k_b
+//      survivors and writes the first k.
+//
+//  fused_wide    (b >= V*NT: few view-rows per bucket; cfg2)
+//      One CTA per row; each thread owns whole vector columns and streams
+//      all s view-rows of them with 128-bit LDGs; the survivors go straight
+//      into the smem pool.
+//
+// Per-element work (both): strict ">" on the exact float value keeps the
+// earliest slot on ties == the reference argmax "first maximum"
+// (approx.py:151-162); -0.0 == +0.0 and subnormals compare exactly (no
+// FTZ, built with -ftz=false).  Stage 2 sorts composite keys descending ==
+// the reference's two stable argsorts (exact.py:130-139).
+//
+// Outside the envelope (contiguous layout, b or n not a multiple of V,
+// misaligned rows, V*k_b > 32, pool > 16384, smem overflow) the generic
+// path (btk_stage1.cu + btk_select.cu) runs instead.
+#include <cooperative_groups.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <cstdio>
+#include <cstdlib>
+
 #include "btk_internal.h"
+#include "btk_sort.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace btk {
-bool fused_supported(const Problem&) { return false; }
-cudaError_t run_fused(const Problem&, void*, int64_t*, cudaStream_t) { return cudaErrorNotSupported; }
+
+namespace {
+
+constexpr int WIDE_NT = 512;
+constexpr int WIDE_U = 8;                  // 16-byte loads in flight per thread
+constexpr int64_t FUSED_POOL_CAP = 16384;  // survivors sorted in smem
+constexpr size_t SMEM_LIMIT = 225 * 1024;  // dynamic; leaves room for static smem
+constexpr int MAX_STAGES = 8;
+constexpr int NUM_SMS = 148;
+
+template <int DT> struct Vec;
+template <> struct Vec<F32> { static constexpr int V = 4; };
+template <> struct Vec<BF16> { static constexpr int V = 8; };
+template <> struct Vec<F16> { static constexpr int V = 8; };
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+// 1-D TMA bulk copy global -> this CTA's shared memory, completion on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// ------------------------------------------------------------------ element helpers
+template <int DT>
+__device__ __forceinline__ void unpack(const uint4& v, float (&f)[Vec<DT>::V]) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  if constexpr (DT == F32) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) f[i] = __uint_as_float(w[i]);
+  } else if constexpr (DT == BF16) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      f[2 * i] = __uint_as_float(w[i] << 16);
+      f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      f[2 * i] = __half2float(__ushort_as_half((unsigned short)(w[i] & 0xFFFFu)));
+      f[2 * i + 1] = __half2float(__ushort_as_half((unsigned short)(w[i] >> 16)));
+    }
+  }
+}
+
+// OR-accumulator whose bit 31 (fp32) / bits 15,31 (16-bit) flag an all-ones exponent.
+template <int DT>
+__device__ __forceinline__ uint32_t nonfinite_bits(const uint4& v) {
+  constexpr uint32_t M = DT == F32 ? 0x7F800000u : (DT == BF16 ? 0x7F807F80u : 0x7C007C00u);
+  constexpr uint32_t A = DT == F32 ? 0x00800000u : (DT == BF16 ? 0x00800080u : 0x04000400u);
+  return ((v.x & M) + A) | ((v.y & M) + A) | ((v.z & M) + A) | ((v.w & M) + A);
+}
+
+template <int DT>
+__device__ __forceinline__ bool nonfinite_hit(uint32_t acc) {
+  return DT == F32 ? (acc & 0x80000000u) != 0 : (acc & 0x80008000u) != 0;
+}
+
+template <int DT>
+__device__ __forceinline__ uint32_t float_bits_to_raw(float f) {
+  const uint32_t u = __float_as_uint(f);
+  if constexpr (DT == F32) return u;
+  else if constexpr (DT == BF16) return u >> 16;
+  else return (uint32_t)__half_as_ushort(__float2half_rn(f));  // exact: f came from a half
+}
+
+// Register queue of the KB best (value, slot) of one bucket, descending.
+template <int KB>
+struct Queue {
+  float v[KB];
+  int t[KB];
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int i = 0; i < KB; ++i) { v[i] = -__int_as_float(0x7F800000); t[i] = -1; }
+  }
+  __device__ __forceinline__ void push(float f, int tt) {
+    if constexpr (KB == 1) {
+      const bool gt = f > v[0];
+      v[0] = gt ? f : v[0];
+      t[0] = gt ? tt : t[0];
+    } else {
+      if (f > v[KB - 1]) {
+#pragma unroll
+        for (int i = KB - 1; i > 0; --i) {
+          const bool up = f > v[i - 1];
+          const bool here = f > v[i];
+          v[i] = up ? v[i - 1] : (here ? f : v[i]);
+          t[i] = up ? t[i - 1] : (here ? tt : t[i]);
+        }
+        const bool top = f > v[0];
+        v[0] = top ? f : v[0];
+        t[0] = top ? tt : t[0];
+      }
+    }
+  }
+};
+
+// Insert a composite key into a descending KB-queue of comps.
+template <int KB>
+__device__ __forceinline__ void comp_push(uint64_t (&best)[KB], uint64_t c) {
+  if (c > best[KB - 1]) {
+#pragma unroll
+    for (int z = KB - 1; z > 0; --z) best[z] = (c > best[z - 1]) ? best[z - 1] : (c > best[z] ? c : best[z]);
+    best[0] = c > best[0] ? c : best[0];
+  }
+}
+
+template <int DT>
+__device__ __forceinline__ uint64_t comp_of(float f, int t, int64_t col, int64_t b,
+                                            const CompGeo& g) {
+  if (t < 0) return 0ull;
+  const uint32_t raw = float_bits_to_raw<DT>(f);
+  return make_comp(vkey<DT>(raw), (uint32_t)(t * b + col), is_negzero<DT>(raw), g);
+}
+
+template <int DT>
+__device__ __forceinline__ void emit_comp(uint64_t c, int64_t pos, const CompGeo& g,
+                                          void* out_vals, int64_t* out_idx) {
+  uint32_t bits;
+  int64_t idx;
+  decode_comp<DT>(c, g, bits, idx);
+  store_bits<DT>(out_vals, pos, bits);
+  out_idx[pos] = idx;
+}
+
+// 64-key bitonic sort (descending) by one warp; keys in sk[0..63].
+__device__ __forceinline__ void warp_sort64_desc(uint64_t* sk) {
+  const int lane = threadIdx.x & 31;
+  uint64_t x[2] = {sk[lane], sk[lane + 32]};
+#pragma unroll
+  for (int size = 2; size <= 64; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride == 32) {
+        const uint64_t hi = x[0] > x[1] ? x[0] : x[1];
+        const uint64_t lo = x[0] > x[1] ? x[1] : x[0];
+        x[0] = hi;
+        x[1] = lo;
+      } else {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = lane + 32 * h;
+          const uint64_t y = __shfl_xor_sync(0xFFFFFFFFu, x[h], stride);
+          const bool lower = (i & stride) == 0;
+          const bool desc = (i & size) == 0;
+          const uint64_t mx = x[h] > y ? x[h] : y;
+          const uint64_t mn = x[h] > y ? y : x[h];
+          x[h] = (lower == desc) ? mx : mn;
+        }
+      }
+    }
+  }
+  sk[lane] = x[0];
+  sk[lane + 32] = x[1];
+}
+
+// Sort the pool (padded to the tile) descending.  MAXI bounds the tile so
+// small-pool kernels keep a small register footprint.
+template <int NT, int MAXI>
+__device__ __forceinline__ void sort_pool(uint64_t* pool, uint32_t* hist, int items, int nbits) {
+  uint32_t* whist = hist;
+  uint32_t* dbase = hist + (NT / 32) * RADIX;
+  uint32_t* dtotal = dbase + RADIX;
+  if constexpr (MAXI <= 8) {
+    switch (items) {
+      case 0: if (threadIdx.x < 32) warp_sort64_desc(pool); break;
+      case 1: block_sort_desc<NT, 1>(pool, whist, dbase, dtotal, 1, nbits); break;
+      case 2: block_sort_desc<NT, 2>(pool, whist, dbase, dtotal, 1, nbits); break;
+      case 4: block_sort_desc<NT, 4>(pool, whist, dbase, dtotal, 1, nbits); break;
+      default: block_sort_desc<NT, 8>(pool, whist, dbase, dtotal, 1, nbits); break;
+    }
+  } else {
+    switch (items) {
+      case 16: block_sort_desc<NT, 16>(pool, whist, dbase, dtotal, 1, nbits); break;
+      default: block_sort_desc<NT, 32>(pool, whist, dbase, dtotal, 1, nbits); break;
+    }
+  }
+  __syncthreads();
+}
+
+int vec_of(int dtype) { return dtype == F32 ? 4 : 8; }
+int esz_of(int dtype) { return dtype == F32 ? 4 : 2; }
+int kb_tmpl(int64_t kb) { return kb <= 1 ? 1 : kb <= 2 ? 2 : kb <= 4 ? 4 : 8; }
+int sort_items_for(int64_t P, int NT) {
+  if (P <= 64) return 0;
+  int items = 1;
+  while ((int64_t)NT * items < P) items <<= 1;
+  return items;
+}
+size_t hist_bytes(int NT) { return (size_t)(NT / 32) * RADIX * 4 + 2 * RADIX * 4; }
+size_t a16(size_t v) { return (v + 127) & ~(size_t)127; }
+
+// Tuning overrides for launch-shape sweeps (unset in production runs).
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return (v && *v) ? std::atoi(v) : dflt;
+}
+
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(addr));
+  return r;
+}
+
+// Per-thread stage-1 state for one vector column (V adjacent buckets).
+// row(v, trel) consumes one 16-byte vector of view-row trel (relative to
+// the CTA's first view-row); spill() writes KB composite keys per bucket.
+// Non-finite detection folds into one FMA per element: x*0 + acc is NaN
+// iff some x was NaN or +-inf.
+template <int DT, int KB>
+struct Scanner {
+  static constexpr int V = Vec<DT>::V;
+  Queue<KB> q[V];
+  float nf[V];
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int e = 0; e < V; ++e) { q[e].init(); nf[e] = 0.f; }
+  }
+  __device__ __forceinline__ void row(const uint4& v, int trel) {
+    float f[V];
+    unpack<DT>(v, f);
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      nf[e] = fmaf(f[e], 0.f, nf[e]);
+      q[e].push(f[e], trel);
+    }
+  }
+  __device__ __forceinline__ bool nonfinite() const {
+    bool bad = false;
+#pragma unroll
+    for (int e = 0; e < V; ++e) bad |= (nf[e] != nf[e]);
+    return bad;
+  }
+  template <int KBS>
+  __device__ __forceinline__ void spill(uint64_t* dst, int g, int64_t b, int64_t t_begin,
+                                        const CompGeo& geo) const {
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      const int64_t col = (int64_t)g * V + e;
+#pragma unroll
+      for (int z = 0; z < KB; ++z) {
+        const int t = q[e].t[z] < 0 ? -1 : (int)(t_begin + q[e].t[z]);
+        dst[col * KBS + z] = comp_of<DT>(q[e].v[z], t, col, b, geo);
+      }
+    }
+  }
+};
+
+// k_b = 1 on 16-bit data: two buckets per 32-bit word, all packed.
+// Per word: HSET2 mask (strict >), two LOP3 bit-selects (value bits kept
+// exactly, so the sign of zero survives) and one HFMA2 for the finite check
+// -> 2 instructions per element.  Slot codes are 16-bit offsets from the
+// CTA's first view-row (planner guarantees < 0xFFFF rows per CTA).
+template <int DT>
+struct Scanner16x2 {
+  static constexpr uint32_t NEG_INF2 = DT == BF16 ? 0xFF80FF80u : 0xFC00FC00u;
+  uint32_t m2[4], c2[4], nf2[4];
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int w = 0; w < 4; ++w) { m2[w] = NEG_INF2; c2[w] = 0xFFFFFFFFu; nf2[w] = 0u; }
+  }
+  __device__ __forceinline__ static uint32_t gt_mask(uint32_t x, uint32_t y) {
+    if constexpr (DT == BF16) {
+      return __hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&x),
+                         *reinterpret_cast<const __nv_bfloat162*>(&y));
+    } else {
+      return __hgt2_mask(*reinterpret_cast<const __half2*>(&x), *reinterpret_cast<const __half2*>(&y));
+    }
+  }
+  __device__ __forceinline__ static uint32_t fma0(uint32_t x, uint32_t acc) {
+    if constexpr (DT == BF16) {
+      __nv_bfloat162 r = __hfma2(*reinterpret_cast<const __nv_bfloat162*>(&x),
+                                 __nv_bfloat162(__float2bfloat16(0.f), __float2bfloat16(0.f)),
+                                 *reinterpret_cast<const __nv_bfloat162*>(&acc));
+      return *reinterpret_cast<uint32_t*>(&r);
+    } else {
+      __half2 r = __hfma2(*reinterpret_cast<const __half2*>(&x), __half2(__float2half(0.f), __float2half(0.f)),
+                          *reinterpret_cast<const __half2*>(&acc));
+      return *reinterpret_cast<uint32_t*>(&r);
+    }
+  }
+  __device__ __forceinline__ void row(const uint4& v, int trel) {
+    const uint32_t code = (uint32_t)trel * 0x10001u;
+    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const uint32_t mask = gt_mask(w4[w], m2[w]);
+      m2[w] = (w4[w] & mask) | (m2[w] & ~mask);
+      c2[w] = (code & mask) | (c2[w] & ~mask);
+      nf2[w] = fma0(w4[w], nf2[w]);
+    }
+  }
+  __device__ __forceinline__ bool nonfinite() const {
+    constexpr uint32_t E = DT == BF16 ? 0x7F80u : 0x7C00u;
+    bool bad = false;
+#pragma unroll
+    for (int w = 0; w < 4; ++w)
+      bad |= ((nf2[w] & 0x7FFFu) > E) || (((nf2[w] >> 16) & 0x7FFFu) > E);
+    return bad;
+  }
+  template <int KBS>
+  __device__ __forceinline__ void spill(uint64_t* dst, int g, int64_t b, int64_t t_begin,
+                                        const CompGeo& geo) const {
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t col = (int64_t)g * 8 + 2 * w + h;
+        const uint32_t raw = (m2[w] >> (16 * h)) & 0xFFFFu;
+        const uint32_t code = (c2[w] >> (16 * h)) & 0xFFFFu;
+        uint64_t c = 0ull;
+        if (code != 0xFFFFu) {
+          const int64_t idx = (t_begin + code) * b + col;
+          c = make_comp(vkey<DT>(raw), (uint32_t)idx, is_negzero<DT>(raw), geo);
+        }
+        dst[col * KBS] = c;
+#pragma unroll
+        for (int z = 1; z < KBS; ++z) dst[col * KBS + z] = 0ull;
+      }
+    }
+  }
+};
+
+template <> struct Scanner<BF16, 1> : Scanner16x2<BF16> {};
+template <> struct Scanner<F16, 1> : Scanner16x2<F16> {};
+
+// ============================================================ narrow (TMA ring, cluster)
+struct NarrowArgs {
+  const void* x;
+  int64_t row_stride;  // elements
+  int64_t m, n, k, b, kb, s;
+  int G, R;            // vector columns, view-row phases per stage
+  int S;               // CTAs per row (cluster size)
+  int T;               // view-rows per ring stage
+  int NS;              // ring stages
+  int sort_items;
+  int64_t P;
+  int last_vec;        // valid vector columns of view-row s-1
+  size_t stage_bytes;  // T * b * esz
+  size_t scratch_off, part_off, pool_off;  // post-scan layout (aliases the ring)
+  CompGeo geo;
+  void* out_vals;
+  int64_t* out_idx;
+  uint32_t* flag;
+};
+
+template <int DT, int KB, int NT, int MAXI>
+__global__ void __launch_bounds__(NT) fused_narrow(NarrowArgs a) {
+  constexpr int V = Vec<DT>::V;
+  constexpr int ESZ = VT<DT>::W / 8;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[MAX_STAGES];
+
+  cg::cluster_group cluster = cg::this_cluster();
+  const int crank = (int)cluster.block_rank();
+  const int64_t row = blockIdx.x / a.S;
+  const int tid = threadIdx.x;
+  const int64_t b = a.b, s = a.s;
+  const uint8_t* rowp = static_cast<const uint8_t*>(a.x) + row * a.row_stride * ESZ;
+  const int64_t t_begin = (s * crank) / a.S, t_end = (s * (crank + 1)) / a.S;
+  const int nstages = (int)((t_end - t_begin + a.T - 1) / a.T);
+
+  if (tid == 0) {
+    for (int i = 0; i < a.NS; ++i) mbar_init(&full[i], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  uint64_t policy = 0;
+  auto issue = [&](int i) {
+    const int slot = i % a.NS;
+    const int64_t t0 = t_begin + (int64_t)i * a.T;
+    const int64_t rows = min((int64_t)a.T, t_end - t0);
+    int64_t elems = rows * b;
+    if (t0 + rows == s) elems -= b - (int64_t)a.last_vec * V;  // ragged final view-row
+    const uint32_t bytes = (uint32_t)(elems * ESZ);
+    // order the consumers' generic-proxy reads of this slot before the
+    // async-proxy (TMA) overwrite
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&full[slot], bytes);
+    bulk_g2s(smem + (size_t)slot * a.stage_bytes, rowp + t0 * b * ESZ, bytes, &full[slot], policy);
+  };
+  if (tid == 0) {
+    policy = evict_first_policy();
+    const int pre = min(a.NS, nstages);
+    for (int i = 0; i < pre; ++i) issue(i);
+  }
+
+  const int G = a.G, R = a.R;
+  const int r = tid / G, g = tid - r * G;
+  const bool active = r < R;
+  Scanner<DT, KB> sc;
+  sc.init();
+  const uint32_t smem_base = smem_u32(smem) + (uint32_t)(g * V * ESZ);
+  const uint32_t row_step = (uint32_t)(R * b * ESZ);
+
+  for (int i = 0; i < nstages; ++i) {
+    const int slot = i % a.NS;
+    mbar_wait(&full[slot], (uint32_t)((i / a.NS) & 1));
+    const int64_t t0 = t_begin + (int64_t)i * a.T;
+    const int rows = (int)min((int64_t)a.T, t_end - t0);
+    // the ragged final view-row (only partially valid) is handled last
+    const bool ragged = (t0 + rows == s) && (a.last_vec < G);
+    const int rows_main = rows - (ragged ? 1 : 0);
+    if (active) {
+      uint32_t addr = smem_base + (uint32_t)(slot * a.stage_bytes) + (uint32_t)(r * b * ESZ);
+      const int trel0 = (int)(t0 - t_begin);
+#pragma unroll 4
+      for (int rr = r; rr < rows_main; rr += R) {
+        sc.row(lds128(addr), trel0 + rr);
+        addr += row_step;
+      }
+      if (ragged && (rows - 1) % R == r && g < a.last_vec)
+        sc.row(lds128(smem_base + (uint32_t)(slot * a.stage_bytes) + (uint32_t)((rows - 1) * b * ESZ)),
+               trel0 + rows - 1);
+    }
+    __syncthreads();  // slot consumed by every thread
+    if (tid == 0 && i + a.NS < nstages) issue(i + a.NS);
+  }
+  const uint32_t bad = sc.nonfinite() ? 1u : 0u;
+
+  // ---- phase queues -> smem (the ring is dead now)
+  uint64_t* scratch = reinterpret_cast<uint64_t*>(smem + a.scratch_off);
+  uint64_t* part = reinterpret_cast<uint64_t*>(smem + a.part_off);
+  uint64_t* pool = reinterpret_cast<uint64_t*>(smem + a.pool_off);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem + a.scratch_off);
+  if (active) sc.template spill<KB>(scratch + (int64_t)r * b * KB, g, b, t_begin, a.geo);
+  __syncthreads();
+  for (int64_t j = tid; j < b; j += NT) {
+    uint64_t best[KB];
+#pragma unroll
+    for (int z = 0; z < KB; ++z) best[z] = 0ull;
+    for (int rr = 0; rr < R; ++rr) {
+#pragma unroll
+      for (int z = 0; z < KB; ++z) comp_push<KB>(best, scratch[((int64_t)rr * b + j) * KB + z]);
+    }
+#pragma unroll
+    for (int z = 0; z < KB; ++z) part[j * KB + z] = best[z];
+  }
+  const bool anybad = __syncthreads_or(bad);
+  if (anybad && tid == 0 && a.flag) atomicOr(a.flag, 1u);
+
+  // ---- cluster merge through DSMEM into the leader's pool
+  if (a.S > 1) cluster.sync();
+  if (crank == 0) {
+    for (int64_t j = tid; j < b; j += NT) {
+      uint64_t best[KB];
+#pragma unroll
+      for (int z = 0; z < KB; ++z) best[z] = part[j * KB + z];
+      for (int c = 1; c < a.S; ++c) {
+        const uint64_t* rp = cluster.map_shared_rank(part, c);
+#pragma unroll
+        for (int z = 0; z < KB; ++z) comp_push<KB>(best, rp[j * KB + z]);
+      }
+#pragma unroll
+      for (int z = 0; z < KB; ++z)
+        if (z < a.kb) pool[j * a.kb + z] = best[z];
+    }
+    const int64_t N = a.sort_items == 0 ? 64 : (int64_t)NT * a.sort_items;
+    for (int64_t p = a.P + tid; p < N; p += NT) pool[p] = 0ull;
+  }
+  if (a.S > 1) cluster.sync();  // remote partials stay alive until read
+  if (crank != 0) return;
+  __syncthreads();
+  sort_pool<NT, MAXI>(pool, hist, a.sort_items, a.geo.nbits);
+  for (int64_t p = tid; p < a.k; p += NT)
+    emit_comp<DT>(pool[p], row * a.k + p, a.geo, a.out_vals, a.out_idx);
+}
+
+// ============================================================ wide (LDG, one CTA per row)
+struct WideArgs {
+  const void* x;
+  int64_t row_stride;
+  int64_t m, n, k, b, kb, s, G;
+  int sort_items;
+  int64_t P;
+  int last_vec;
+  size_t pool_off;
+  CompGeo geo;
+  void* out_vals;
+  int64_t* out_idx;
+  uint32_t* flag;
+};
+
+template <int DT, int KB, int NT, int U, int MAXI>
+__global__ void __launch_bounds__(NT, 1) fused_wide(WideArgs a) {
+  constexpr int V = Vec<DT>::V;
+  constexpr int ESZ = VT<DT>::W / 8;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* pool = reinterpret_cast<uint64_t*>(smem + a.pool_off);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem);
+  const int64_t row = blockIdx.x;
+  const uint8_t* rowp = static_cast<const uint8_t*>(a.x) + row * a.row_stride * ESZ;
+  const int64_t b = a.b, s = a.s;
+  const int tid = threadIdx.x;
+  uint32_t bad = 0;
+  for (int64_t g = tid; g < a.G; g += NT) {
+    Queue<KB> q[V];
+#pragma unroll
+    for (int e = 0; e < V; ++e) q[e].init();
+    const uint8_t* colp = rowp + g * V * ESZ;
+    const int64_t s_eff = (g < a.last_vec) ? s : s - 1;  // ragged final view-row
+    for (int64_t t0 = 0; t0 < s_eff; t0 += U) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t t = t0 + u;
+        v[u] = (t < s_eff) ? ldg_stream(colp + t * b * ESZ) : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t t = t0 + u;
+        if (t < s_eff) {
+          bad |= nonfinite_bits<DT>(v[u]);
+          float f[V];
+          unpack<DT>(v[u], f);
+#pragma unroll
+          for (int e = 0; e < V; ++e) q[e].push(f[e], (int)t);
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      const int64_t col = g * V + e;
+#pragma unroll
+      for (int z = 0; z < KB; ++z)
+        if (z < a.kb) pool[col * a.kb + z] = comp_of<DT>(q[e].v[z], q[e].t[z], col, b, a.geo);
+    }
+  }
+  const int64_t N = a.sort_items == 0 ? 64 : (int64_t)NT * a.sort_items;
+  for (int64_t p = a.P + tid; p < N; p += NT) pool[p] = 0ull;
+  if (__syncthreads_or(nonfinite_hit<DT>(bad)) && tid == 0 && a.flag) atomicOr(a.flag, 1u);
+  sort_pool<NT, MAXI>(pool, hist, a.sort_items, a.geo.nbits);
+  for (int64_t p = tid; p < a.k; p += NT)
+    emit_comp<DT>(pool[p], row * a.k + p, a.geo, a.out_vals, a.out_idx);
+}
+
+// ============================================================ planning
+enum Kind { NONE = 0, NARROW = 1, WIDE = 2 };
+
+struct Plan {
+  Kind kind = NONE;
+  int nt = 0;
+  size_t smem = 0;
+  NarrowArgs na{};
+  WideArgs wa{};
+};
+
+bool common_envelope(const Problem& p) {
+  if (p.layout != 0 || p.kb > 8) return false;
+  const int V = vec_of(p.dtype), esz = esz_of(p.dtype);
+  if (V * p.kb > 32) return false;  // register queue budget (V buckets x k_b)
+  if (p.b % V || p.n % V) return false;
+  if ((reinterpret_cast<uintptr_t>(p.x) & 15) || ((p.row_stride * esz) & 15)) return false;
+  if (p.b * p.kb > FUSED_POOL_CAP) return false;
+  return true;
+}
+
+bool plan_narrow(const Problem& p, Plan& pl) {
+  const int V = vec_of(p.dtype), esz = esz_of(p.dtype);
+  const int64_t G = p.b / V, s = (p.n + p.b - 1) / p.b, P = p.b * p.kb;
+  const int NT = G <= 16 ? 128 : 256;
+  if (G > NT) return false;
+  NarrowArgs& a = pl.na;
+  a.x = p.x; a.row_stride = p.row_stride;
+  a.m = p.m; a.n = p.n; a.k = p.k; a.b = p.b; a.kb = p.kb; a.s = s;
+  a.G = (int)G;
+  a.R = (int)(NT / G);
+  const int64_t vrow_bytes = p.b * esz;
+  // stage: ~16 KB of whole view-rows, a multiple of R rows when possible
+  int64_t T = std::max<int64_t>(1, ((int64_t)env_int("BTK_STAGE_KB", 16) * 1024) / vrow_bytes);
+  if (T >= a.R) T = (T / a.R) * a.R;
+  if (T * vrow_bytes > 64 * 1024) return false;
+  a.T = (int)T;
+  a.stage_bytes = (size_t)(T * vrow_bytes);
+  a.last_vec = (int)((p.n - (s - 1) * p.b) / V);
+  a.P = P;
+  a.sort_items = sort_items_for(P, NT);
+  const int64_t N = a.sort_items == 0 ? 64 : (int64_t)NT * a.sort_items;
+  const int kbt = kb_tmpl(p.kb);
+  const size_t scratch = (size_t)a.R * p.b * kbt * 8;
+  const size_t regA = a16(std::max(scratch, hist_bytes(NT)));
+  a.scratch_off = 0;
+  a.part_off = regA;
+  a.pool_off = regA + a16((size_t)p.b * kbt * 8);
+  const size_t post = a.pool_off + (size_t)N * 8;
+  // cluster size: split rows until the grid fills one resident wave
+  const int64_t row_bytes = p.n * esz;
+  int S = 1;
+  int NS = 1;
+  size_t smem = 0;
+  const int force_s = env_int("BTK_S", 0);
+  for (int cand = 8; cand >= 1; cand >>= 1) {
+    if (cand > s) continue;
+    if (force_s && cand != force_s) continue;
+    const int64_t range_rows = (s + cand - 1) / cand;
+    if (range_rows >= 0xFFFF) continue;  // 16-bit slot codes of the packed scanner
+    const int64_t stages = (range_rows + T - 1) / T;
+    const int ns = (int)std::min<int64_t>(std::min<int64_t>(stages, env_int("BTK_NS", 2)), MAX_STAGES);
+    const size_t sm = std::max(post, (size_t)ns * a.stage_bytes);
+    const int per_sm_smem = (int)(SMEM_LIMIT / (sm + 1024));
+    const int per_sm = std::min(per_sm_smem, 2048 / NT);
+    if (per_sm < 1) continue;
+    const int64_t slots = (int64_t)per_sm * NUM_SMS;
+    if (p.m * cand <= slots || cand == 1) {
+      // prefer the largest split that still fits one wave when rows are few
+      if (p.m * cand <= slots && (row_bytes / cand) >= 16 * 1024) {
+        S = cand; NS = ns; smem = sm;
+        break;
+      }
+      if (cand == 1 || force_s) { S = cand; NS = ns; smem = sm; }
+    }
+  }
+  if (smem == 0 || smem > SMEM_LIMIT) return false;
+  a.S = S;
+  a.NS = NS;
+  a.geo = p.geo;
+  a.flag = p.flag;
+  pl.kind = NARROW;
+  pl.nt = NT;
+  pl.smem = smem;
+  return true;
+}
+
+bool plan_wide(const Problem& p, Plan& pl) {
+  const int V = vec_of(p.dtype), esz = esz_of(p.dtype);
+  (void)esz;
+  const int64_t G = p.b / V, s = (p.n + p.b - 1) / p.b, P = p.b * p.kb;
+  WideArgs& a = pl.wa;
+  a.x = p.x; a.row_stride = p.row_stride;
+  a.m = p.m; a.n = p.n; a.k = p.k; a.b = p.b; a.kb = p.kb; a.s = s; a.G = G;
+  a.P = P;
+  a.last_vec = (int)((p.n - (s - 1) * p.b) / V);
+  a.sort_items = sort_items_for(P, WIDE_NT);
+  const int64_t N = a.sort_items == 0 ? 64 : (int64_t)WIDE_NT * a.sort_items;
+  a.pool_off = a16(hist_bytes(WIDE_NT));
+  a.geo = p.geo;
+  a.flag = p.flag;
+  pl.smem = a.pool_off + (size_t)N * 8;
+  pl.kind = WIDE;
+  pl.nt = WIDE_NT;
+  return pl.smem <= SMEM_LIMIT;
+}
+
+bool make_plan(const Problem& p, Plan& pl) {
+  if (!common_envelope(p)) return false;
+  if (plan_narrow(p, pl)) return true;
+  return plan_wide(p, pl);
+}
+
+template <int DT, int KB>
+cudaError_t launch_narrow(const Plan& pl, cudaStream_t st) {
+  const NarrowArgs& a = pl.na;
+  void (*kern)(NarrowArgs);
+  if (pl.nt == 128) kern = a.sort_items <= 8 ? fused_narrow<DT, KB, 128, 8> : fused_narrow<DT, KB, 128, 32>;
+  else kern = a.sort_items <= 8 ? fused_narrow<DT, KB, 256, 8> : fused_narrow<DT, KB, 256, 32>;
+  cudaError_t e = ensure_smem_attr((const void*)kern, pl.smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(a.m * a.S));
+  cfg.blockDim = dim3(pl.nt);
+  cfg.dynamicSmemBytes = pl.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = a.S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+template <int DT, int KB>
+cudaError_t launch_wide(const Plan& pl, cudaStream_t st) {
+  const WideArgs& a = pl.wa;
+  auto kern = a.sort_items <= 8 ? fused_wide<DT, KB, WIDE_NT, WIDE_U, 8>
+                                : fused_wide<DT, KB, WIDE_NT, WIDE_U, 32>;
+  cudaError_t e = ensure_smem_attr((const void*)kern, pl.smem);
+  if (e != cudaSuccess) return e;
+  kern<<<(unsigned)a.m, WIDE_NT, pl.smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int DT, int KB>
+cudaError_t launch_any(const Plan& pl, cudaStream_t st) {
+  return pl.kind == NARROW ? launch_narrow<DT, KB>(pl, st) : launch_wide<DT, KB>(pl, st);
+}
+
+template <int DT>
+cudaError_t launch_kb(const Plan& pl, int64_t kb, cudaStream_t st) {
+  if (kb <= 1) return launch_any<DT, 1>(pl, st);
+  if (kb <= 2) return launch_any<DT, 2>(pl, st);
+  if (kb <= 4) return launch_any<DT, 4>(pl, st);
+  if constexpr (DT == F32) return launch_any<DT, 8>(pl, st);
+  return cudaErrorNotSupported;
+}
+
+}  // namespace
+
+bool fused_supported(const Problem& p) {
+  Plan pl;
+  return make_plan(p, pl);
+}
+
+cudaError_t run_fused(const Problem& p, void* out_vals, int64_t* out_idx, cudaStream_t st) {
+  Plan pl;
+  if (!make_plan(p, pl)) return cudaErrorNotSupported;
+  pl.na.out_vals = pl.wa.out_vals = out_vals;
+  pl.na.out_idx = pl.wa.out_idx = out_idx;
+  cudaError_t e = cudaErrorInvalidValue;
+  switch (p.dtype) {
+    case F32: e = launch_kb<F32>(pl, p.kb, st); break;
+    case BF16: e = launch_kb<BF16>(pl, p.kb, st); break;
+    case F16: e = launch_kb<F16>(pl, p.kb, st); break;
+  }
+  if (e != cudaSuccess && env_int("BTK_DEBUG", 0))
+    fprintf(stderr, "[btk] fused launch failed: %s kind=%d nt=%d smem=%zu S=%d NS=%d T=%d R=%d G=%d m=%lld\n",
+            cudaGetErrorString(e), (int)pl.kind, pl.nt, pl.smem, pl.na.S, pl.na.NS, pl.na.T, pl.na.R,
+            pl.na.G, (long long)p.m);
+  return e;
+}
+
 }  // namespace btk

@@ -31,7 +31,7 @@ struct K2Args {
 // Opt a kernel into >48 KB dynamic smem once per device (never during
 // stream capture, where the warm-up call has already done it).
 inline cudaError_t ensure_smem_attr(const void* fn, size_t bytes) {
-  if (bytes <= 48 * 1024) return cudaSuccess;
+  if (bytes == 0) return cudaSuccess;
   static thread_local const void* done_fn[64];
   static thread_local int done_dev[64];
   static thread_local int n_done = 0;
@@ -39,7 +39,9 @@ inline cudaError_t ensure_smem_attr(const void* fn, size_t bytes) {
   cudaGetDevice(&dev);
   for (int i = 0; i < n_done; ++i)
     if (done_fn[i] == fn && done_dev[i] == dev) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  // opt in to the full 227 KB once; the per-launch size still sets occupancy
+  (void)bytes;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
   if (e == cudaSuccess && n_done < 64) { done_fn[n_done] = fn; done_dev[n_done] = dev; ++n_done; }
   return e;
 }
