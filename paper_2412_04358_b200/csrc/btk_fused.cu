@@ -41,6 +41,7 @@
 #include <cstdlib>
 
 #include "btk_internal.h"
+#include "btk_rank.cuh"
 #include "btk_sort.cuh"
 
 namespace cg = cooperative_groups;
@@ -107,6 +108,12 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Outputs are written only after the predecessor grid completed (we already
+// waited before the first read, so this is a no-op kept as the hook).
+__device__ __forceinline__ void pdl_wait_writes() {}
 
 __device__ __forceinline__ uint4 ldg_stream(const void* p) {
   uint4 r;
@@ -249,46 +256,77 @@ __device__ __forceinline__ void warp_sort64_desc(uint64_t* sk) {
   sk[lane + 32] = x[1];
 }
 
-// Sort the pool (padded to the tile) descending.  MAXI bounds the tile so
-// small-pool kernels keep a small register footprint.
-template <int NT, int MAXI>
-__device__ __forceinline__ void sort_pool(uint64_t* pool, uint32_t* hist, int items, int nbits) {
-  uint32_t* whist = hist;
-  uint32_t* dbase = hist + (NT / 32) * RADIX;
-  uint32_t* dtotal = dbase + RADIX;
-  if constexpr (MAXI <= 8) {
-    switch (items) {
-      case 0: if (threadIdx.x < 32) warp_sort64_desc(pool); break;
-      case 1: block_sort_desc<NT, 1>(pool, whist, dbase, dtotal, 1, nbits); break;
-      case 2: block_sort_desc<NT, 2>(pool, whist, dbase, dtotal, 1, nbits); break;
-      case 4: block_sort_desc<NT, 4>(pool, whist, dbase, dtotal, 1, nbits); break;
-      default: block_sort_desc<NT, 8>(pool, whist, dbase, dtotal, 1, nbits); break;
-    }
-  } else {
-    switch (items) {
-      case 16: block_sort_desc<NT, 16>(pool, whist, dbase, dtotal, 1, nbits); break;
-      default: block_sort_desc<NT, 32>(pool, whist, dbase, dtotal, 1, nbits); break;
-    }
+// Stage 2 of one row's pool: the P survivors (ITEMS == 0, P <= 64: warp
+// bitonic sort of a zero-padded 64-key tile; else the bucketing/rank engine
+// of btk_rank.cuh with ITEMS >= P/NT keys per thread), then the canonical
+// write of the first k.  `aux` is the engine's shared-memory scratch
+// (rank_aux_bytes).  ITEMS is exact per kernel instance so the register
+// budget of small-pool kernels is not set by the largest pools.
+__device__ __forceinline__ RankSmem rank_smem(uint64_t* pool, uint8_t* aux, int k, int lognb, int nt) {
+  RankSmem S;
+  S.pool = pool;
+  S.hist = reinterpret_cast<uint32_t*>(aux);
+  aux += ((size_t)((1 << lognb) + 2) * 4 + 127) / 128 * 128;
+  S.inv = reinterpret_cast<uint16_t*>(aux);
+  aux += ((size_t)k * 2 + 127) / 128 * 128;
+  S.work = reinterpret_cast<int2*>(aux);
+  aux += (size_t)RS_WORK * 8;
+  S.red = reinterpret_cast<uint64_t*>(aux);
+  aux += (size_t)(nt / 32) * 24;
+  S.ctl = reinterpret_cast<int*>(aux);
+  return S;
+}
+
+template <int DT, int NT, int ITEMS>
+__device__ __forceinline__ void stage2_emit(uint64_t* pool, uint8_t* aux, int64_t P, int64_t k,
+                                            int lognb, int64_t row, const CompGeo& geo,
+                                            void* out_vals, int64_t* out_idx) {
+  if constexpr (ITEMS == 0) {
+    for (int64_t p = P + threadIdx.x; p < 64; p += NT) pool[p] = 0ull;
+    __syncthreads();
+    if (threadIdx.x < 32) warp_sort64_desc(pool);
+    __syncthreads();
+    pdl_wait_writes();
+    for (int64_t p = threadIdx.x; p < k; p += NT) emit_comp<DT>(pool[p], row * k + p, geo, out_vals, out_idx);
+    return;
   }
-  __syncthreads();
+  else {
+    const RankSmem S = rank_smem(pool, aux, (int)k, lognb, NT);
+    rank_select_sort<DT, NT, ITEMS>(S, (int)P, (int)k, lognb, geo.ib);
+    pdl_wait_writes();
+    for (int64_t q = threadIdx.x; q < k; q += NT)
+      emit_comp<DT>(rs_key(pool, S.inv[q]), row * k + q, geo, out_vals, out_idx);
+  }
 }
 
 int vec_of(int dtype) { return dtype == F32 ? 4 : 8; }
 int esz_of(int dtype) { return dtype == F32 ? 4 : 2; }
 int kb_tmpl(int64_t kb) { return kb <= 1 ? 1 : kb <= 2 ? 2 : kb <= 4 ? 4 : 8; }
+// Engine keys per thread, rounded up to the instantiated set {0, 2, 8, 32}.
 int sort_items_for(int64_t P, int NT) {
   if (P <= 64) return 0;
-  int items = 1;
-  while ((int64_t)NT * items < P) items <<= 1;
-  return items;
+  if (P <= 2 * (int64_t)NT) return 2;
+  if (P <= 8 * (int64_t)NT) return 8;
+  return 32;
 }
-size_t hist_bytes(int NT) { return (size_t)(NT / 32) * RADIX * 4 + 2 * RADIX * 4; }
+// Stage-2 shared memory after the pool's P keys.
+size_t stage2_bytes(int64_t P, int64_t k, int NT) {
+  if (P <= 64) return 64 * 8;
+  return ((size_t)P * 8 + 127) / 128 * 128 + rank_aux_bytes(NT, rank_lognb(P), k);
+}
 size_t a16(size_t v) { return (v + 127) & ~(size_t)127; }
 
 // Tuning overrides for launch-shape sweeps (unset in production runs).
 int env_int(const char* name, int dflt) {
   const char* v = std::getenv(name);
   return (v && *v) ? std::atoi(v) : dflt;
+}
+
+// Programmatic dependent launch: off by default (measured neutral for a
+// plain read kernel and slower for the cluster kernel); BTK_PDL=1 enables.
+bool pdl_enabled() {
+  static const int v = env_int("BTK_PDL", 0);
+  return v != 0;
 }
 
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
@@ -434,14 +472,15 @@ struct NarrowArgs {
   int64_t P;
   int last_vec;        // valid vector columns of view-row s-1
   size_t stage_bytes;  // T * b * esz
-  size_t scratch_off, part_off, pool_off;  // post-scan layout (aliases the ring)
+  size_t scratch_off, part_off, pool_off, aux_off;  // post-scan layout (aliases the ring)
+  int lognb;
   CompGeo geo;
   void* out_vals;
   int64_t* out_idx;
   uint32_t* flag;
 };
 
-template <int DT, int KB, int NT, int MAXI>
+template <int DT, int KB, int NT, int ITEMS>
 __global__ void __launch_bounds__(NT) fused_narrow(NarrowArgs a) {
   constexpr int V = Vec<DT>::V;
   constexpr int ESZ = VT<DT>::W / 8;
@@ -461,6 +500,11 @@ __global__ void __launch_bounds__(NT) fused_narrow(NarrowArgs a) {
     for (int i = 0; i < a.NS; ++i) mbar_init(&full[i], 1);
     fence_barrier_init();
   }
+  // Programmatic dependent launch: let the next launch in the stream get
+  // resident during our tail, and wait for our predecessor to finish (its
+  // writes may be our input) before the first read.
+  pdl_trigger();
+  pdl_wait();
   __syncthreads();
 
   uint64_t policy = 0;
@@ -520,7 +564,6 @@ __global__ void __launch_bounds__(NT) fused_narrow(NarrowArgs a) {
   uint64_t* scratch = reinterpret_cast<uint64_t*>(smem + a.scratch_off);
   uint64_t* part = reinterpret_cast<uint64_t*>(smem + a.part_off);
   uint64_t* pool = reinterpret_cast<uint64_t*>(smem + a.pool_off);
-  uint32_t* hist = reinterpret_cast<uint32_t*>(smem + a.scratch_off);
   if (active) sc.template spill<KB>(scratch + (int64_t)r * b * KB, g, b, t_begin, a.geo);
   __syncthreads();
   for (int64_t j = tid; j < b; j += NT) {
@@ -553,15 +596,12 @@ __global__ void __launch_bounds__(NT) fused_narrow(NarrowArgs a) {
       for (int z = 0; z < KB; ++z)
         if (z < a.kb) pool[j * a.kb + z] = best[z];
     }
-    const int64_t N = a.sort_items == 0 ? 64 : (int64_t)NT * a.sort_items;
-    for (int64_t p = a.P + tid; p < N; p += NT) pool[p] = 0ull;
   }
   if (a.S > 1) cluster.sync();  // remote partials stay alive until read
   if (crank != 0) return;
   __syncthreads();
-  sort_pool<NT, MAXI>(pool, hist, a.sort_items, a.geo.nbits);
-  for (int64_t p = tid; p < a.k; p += NT)
-    emit_comp<DT>(pool[p], row * a.k + p, a.geo, a.out_vals, a.out_idx);
+  stage2_emit<DT, NT, ITEMS>(pool, smem + a.aux_off, a.P, a.k, a.lognb, row, a.geo, a.out_vals,
+                            a.out_idx);
 }
 
 // ============================================================ wide (LDG, one CTA per row)
@@ -572,25 +612,27 @@ struct WideArgs {
   int sort_items;
   int64_t P;
   int last_vec;
-  size_t pool_off;
+  size_t pool_off, aux_off;
+  int lognb;
   CompGeo geo;
   void* out_vals;
   int64_t* out_idx;
   uint32_t* flag;
 };
 
-template <int DT, int KB, int NT, int U, int MAXI>
+template <int DT, int KB, int NT, int U, int ITEMS>
 __global__ void __launch_bounds__(NT, 1) fused_wide(WideArgs a) {
   constexpr int V = Vec<DT>::V;
   constexpr int ESZ = VT<DT>::W / 8;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* pool = reinterpret_cast<uint64_t*>(smem + a.pool_off);
-  uint32_t* hist = reinterpret_cast<uint32_t*>(smem);
   const int64_t row = blockIdx.x;
   const uint8_t* rowp = static_cast<const uint8_t*>(a.x) + row * a.row_stride * ESZ;
   const int64_t b = a.b, s = a.s;
   const int tid = threadIdx.x;
   uint32_t bad = 0;
+  pdl_trigger();
+  pdl_wait();
   for (int64_t g = tid; g < a.G; g += NT) {
     Queue<KB> q[V];
 #pragma unroll
@@ -624,12 +666,9 @@ __global__ void __launch_bounds__(NT, 1) fused_wide(WideArgs a) {
         if (z < a.kb) pool[col * a.kb + z] = comp_of<DT>(q[e].v[z], q[e].t[z], col, b, a.geo);
     }
   }
-  const int64_t N = a.sort_items == 0 ? 64 : (int64_t)NT * a.sort_items;
-  for (int64_t p = a.P + tid; p < N; p += NT) pool[p] = 0ull;
   if (__syncthreads_or(nonfinite_hit<DT>(bad)) && tid == 0 && a.flag) atomicOr(a.flag, 1u);
-  sort_pool<NT, MAXI>(pool, hist, a.sort_items, a.geo.nbits);
-  for (int64_t p = tid; p < a.k; p += NT)
-    emit_comp<DT>(pool[p], row * a.k + p, a.geo, a.out_vals, a.out_idx);
+  stage2_emit<DT, NT, ITEMS>(pool, smem + a.aux_off, a.P, a.k, a.lognb, row, a.geo, a.out_vals,
+                            a.out_idx);
 }
 
 // ============================================================ planning
@@ -673,14 +712,16 @@ bool plan_narrow(const Problem& p, Plan& pl) {
   a.last_vec = (int)((p.n - (s - 1) * p.b) / V);
   a.P = P;
   a.sort_items = sort_items_for(P, NT);
-  const int64_t N = a.sort_items == 0 ? 64 : (int64_t)NT * a.sort_items;
+  if (a.sort_items > 32) return false;  // engine keys per thread
+  a.lognb = rank_lognb(P);
   const int kbt = kb_tmpl(p.kb);
   const size_t scratch = (size_t)a.R * p.b * kbt * 8;
-  const size_t regA = a16(std::max(scratch, hist_bytes(NT)));
+  const size_t regA = a16(scratch);
   a.scratch_off = 0;
   a.part_off = regA;
   a.pool_off = regA + a16((size_t)p.b * kbt * 8);
-  const size_t post = a.pool_off + (size_t)N * 8;
+  a.aux_off = a.pool_off + (P <= 64 ? 64 * 8 : a16((size_t)P * 8));
+  const size_t post = a.pool_off + stage2_bytes(P, p.k, NT);
   // cluster size: split rows until the grid fills one resident wave
   const int64_t row_bytes = p.n * esz;
   int S = 1;
@@ -729,11 +770,13 @@ bool plan_wide(const Problem& p, Plan& pl) {
   a.P = P;
   a.last_vec = (int)((p.n - (s - 1) * p.b) / V);
   a.sort_items = sort_items_for(P, WIDE_NT);
-  const int64_t N = a.sort_items == 0 ? 64 : (int64_t)WIDE_NT * a.sort_items;
-  a.pool_off = a16(hist_bytes(WIDE_NT));
+  if (a.sort_items > 32) return false;
+  a.lognb = rank_lognb(P);
+  a.pool_off = 0;
+  a.aux_off = P <= 64 ? 64 * 8 : a16((size_t)P * 8);
   a.geo = p.geo;
   a.flag = p.flag;
-  pl.smem = a.pool_off + (size_t)N * 8;
+  pl.smem = stage2_bytes(P, p.k, WIDE_NT);
   pl.kind = WIDE;
   pl.nt = WIDE_NT;
   return pl.smem <= SMEM_LIMIT;
@@ -749,8 +792,12 @@ template <int DT, int KB>
 cudaError_t launch_narrow(const Plan& pl, cudaStream_t st) {
   const NarrowArgs& a = pl.na;
   void (*kern)(NarrowArgs);
-  if (pl.nt == 128) kern = a.sort_items <= 8 ? fused_narrow<DT, KB, 128, 8> : fused_narrow<DT, KB, 128, 32>;
-  else kern = a.sort_items <= 8 ? fused_narrow<DT, KB, 256, 8> : fused_narrow<DT, KB, 256, 32>;
+  switch (a.sort_items) {
+    case 0: kern = pl.nt == 128 ? fused_narrow<DT, KB, 128, 0> : fused_narrow<DT, KB, 256, 0>; break;
+    case 2: kern = pl.nt == 128 ? fused_narrow<DT, KB, 128, 2> : fused_narrow<DT, KB, 256, 2>; break;
+    case 8: kern = pl.nt == 128 ? fused_narrow<DT, KB, 128, 8> : fused_narrow<DT, KB, 256, 8>; break;
+    default: kern = pl.nt == 128 ? fused_narrow<DT, KB, 128, 32> : fused_narrow<DT, KB, 256, 32>; break;
+  }
   cudaError_t e = ensure_smem_attr((const void*)kern, pl.smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
@@ -758,25 +805,41 @@ cudaError_t launch_narrow(const Plan& pl, cudaStream_t st) {
   cfg.blockDim = dim3(pl.nt);
   cfg.dynamicSmemBytes = pl.smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = a.S;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 template <int DT, int KB>
 cudaError_t launch_wide(const Plan& pl, cudaStream_t st) {
   const WideArgs& a = pl.wa;
-  auto kern = a.sort_items <= 8 ? fused_wide<DT, KB, WIDE_NT, WIDE_U, 8>
-                                : fused_wide<DT, KB, WIDE_NT, WIDE_U, 32>;
+  void (*kern)(WideArgs);
+  switch (a.sort_items) {
+    case 0: kern = fused_wide<DT, KB, WIDE_NT, WIDE_U, 0>; break;
+    case 2: kern = fused_wide<DT, KB, WIDE_NT, WIDE_U, 2>; break;
+    case 8: kern = fused_wide<DT, KB, WIDE_NT, WIDE_U, 8>; break;
+    default: kern = fused_wide<DT, KB, WIDE_NT, WIDE_U, 32>; break;
+  }
   cudaError_t e = ensure_smem_attr((const void*)kern, pl.smem);
   if (e != cudaSuccess) return e;
-  kern<<<(unsigned)a.m, WIDE_NT, pl.smem, st>>>(a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)a.m);
+  cfg.blockDim = dim3(WIDE_NT);
+  cfg.dynamicSmemBytes = pl.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 template <int DT, int KB>

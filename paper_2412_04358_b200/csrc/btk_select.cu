@@ -14,6 +14,7 @@
 //                    the smem sort if kk fits, else k2_global_lsd (stable
 //                    LSD passes through a global ping-pong buffer).
 #include "btk_internal.h"
+#include "btk_rank.cuh"
 #include "btk_sort.cuh"
 
 namespace btk {
@@ -29,30 +30,40 @@ __device__ __forceinline__ void emit(uint64_t c, int64_t pos, const CompGeo& g, 
 }
 
 // ---------------------------------------------------------------------------
+// One CTA per segment of L <= NT*ITEMS keys: keys into shared memory, the
+// bucketing/rank engine (btk_rank.cuh) finds the kk largest in order.
 template <int DT, int NT, int ITEMS, bool DECODE>
 __global__ void __launch_bounds__(NT) k2_small(const uint64_t* __restrict__ in, int64_t in_stride,
                                                int64_t L, int64_t kk, uint64_t* __restrict__ out_keys,
                                                void* __restrict__ out_vals,
                                                int64_t* __restrict__ out_idx, int64_t out_stride,
-                                               CompGeo g) {
-  constexpr int N = NT * ITEMS;
-  constexpr int NW = NT / 32;
+                                               CompGeo g, int lognb) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw);
-  uint32_t* whist = reinterpret_cast<uint32_t*>(sk + N);
-  uint32_t* dbase = whist + NW * RADIX;
-  uint32_t* dtotal = dbase + RADIX;
+  uint8_t* aux = smem_raw + ((size_t)L * 8 + 127) / 128 * 128;
+  RankSmem S;
+  S.pool = sk;
+  S.hist = reinterpret_cast<uint32_t*>(aux);
+  aux += ((size_t)((1 << lognb) + 2) * 4 + 127) / 128 * 128;
+  S.inv = reinterpret_cast<uint16_t*>(aux);
+  aux += ((size_t)kk * 2 + 127) / 128 * 128;
+  S.work = reinterpret_cast<int2*>(aux);
+  aux += (size_t)RS_WORK * 8;
+  S.red = reinterpret_cast<uint64_t*>(aux);
+  aux += (size_t)(NT / 32) * 24;
+  S.ctl = reinterpret_cast<int*>(aux);
   const int64_t seg = blockIdx.x;
   const uint64_t* src = in + seg * in_stride;
-  for (int p = threadIdx.x; p < N; p += NT) sk[p] = (p < L) ? src[p] : 0ull;
+  for (int p = threadIdx.x; p < L; p += NT) sk[p] = src[p];
   __syncthreads();
-  // bit 0 (negzero) never decides the order of unique comps
-  block_sort_desc<NT, ITEMS>(sk, whist, dbase, dtotal, 1, g.nbits);
+  rank_select_sort<DT, NT, ITEMS>(S, (int)L, (int)kk, lognb, g.ib);
+  // fewer than kk non-empty keys (only via empty slots): pad with 0 = "empty"
   for (int p = threadIdx.x; p < kk; p += NT) {
+    const uint64_t c = rs_key(sk, S.inv[p]);
     if constexpr (DECODE) {
-      emit<DT>(sk[p], seg * out_stride + p, g, out_vals, out_idx);
+      emit<DT>(c, seg * out_stride + p, g, out_vals, out_idx);
     } else {
-      out_keys[seg * out_stride + p] = sk[p];
+      out_keys[seg * out_stride + p] = c;
     }
   }
 }
@@ -204,32 +215,27 @@ __global__ void k2_decode(const uint64_t* __restrict__ in, int64_t in_stride, in
 
 // ---------------------------------------------------------------------------
 // Host dispatch.
-template <int NT, int ITEMS>
-static constexpr size_t small_smem() {
-  return (size_t)NT * ITEMS * 8 + (size_t)(NT / 32) * RADIX * 4 + 2 * RADIX * 4;
-}
-
 template <int DT, int NT, int ITEMS, bool DECODE>
 static cudaError_t launch_small(const K2Args& a, cudaStream_t st) {
   auto kern = k2_small<DT, NT, ITEMS, DECODE>;
-  constexpr size_t sm = small_smem<NT, ITEMS>();
+  const int lognb = rank_lognb(a.L);
+  const size_t sm = ((size_t)a.L * 8 + 127) / 128 * 128 + rank_aux_bytes(NT, lognb, a.kk);
   cudaError_t e = ensure_smem_attr((const void*)kern, sm);
   if (e != cudaSuccess) return e;
   if (a.nseg == 0) return cudaSuccess;
   kern<<<(unsigned)a.nseg, NT, sm, st>>>(a.in, a.in_stride, a.L, a.kk, a.out_keys, a.out_vals,
-                                         a.out_idx, a.out_stride, a.geo);
+                                         a.out_idx, a.out_stride, a.geo, lognb);
   return cudaGetLastError();
 }
 
 template <int DT, bool DECODE>
 static cudaError_t run_small(const K2Args& a, cudaStream_t st) {
   const int64_t L = a.L;
-  if (L <= 256) return launch_small<DT, 64, 4, DECODE>(a, st);
-  if (L <= 1024) return launch_small<DT, 128, 8, DECODE>(a, st);
-  if (L <= 2048) return launch_small<DT, 256, 8, DECODE>(a, st);
+  if (L <= 64) return launch_small<DT, 64, 1, DECODE>(a, st);
+  if (L <= 256) return launch_small<DT, 128, 2, DECODE>(a, st);
+  if (L <= 1024) return launch_small<DT, 256, 4, DECODE>(a, st);
   if (L <= 4096) return launch_small<DT, 512, 8, DECODE>(a, st);
-  if (L <= 8192) return launch_small<DT, 1024, 8, DECODE>(a, st);
-  return launch_small<DT, 1024, 16, DECODE>(a, st);
+  return launch_small<DT, 512, 32, DECODE>(a, st);
 }
 
 template <int DT, bool DECODE>
