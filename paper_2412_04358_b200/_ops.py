@@ -88,8 +88,10 @@ def as_rows(t: torch.Tensor, dim: int = -1):
 
 
 def workspace(nbytes: int, device) -> torch.Tensor:
-    # torch's caching allocator returns >= 512-byte aligned blocks
-    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+    """Zero-filled device workspace (include/btk.h: zero before first use;
+    the library leaves it zero).  torch's caching allocator returns
+    >= 512-byte aligned blocks."""
+    return torch.zeros(max(int(nbytes), 1), dtype=torch.uint8, device=device)
 
 
 def stream_handle(device) -> int:

@@ -128,10 +128,17 @@ int64_t btk_stage1_count(int64_t n, int64_t b, int64_t kb, int layout) {
 
 size_t btk_workspace_bytes(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, int dtype,
                            int layout) {
-  (void)dtype;
-  (void)layout;
-  if (btk_validate(m, n, k, b, kb) != BTK_OK) return 0;
-  return plan_generic(m, n, k, b, kb).total();
+  if (btk_validate(m, n, k, b, kb) != BTK_OK || !dtype_ok(dtype)) return 0;
+  // the fused plan depends on alignment only through x / row_stride; size it
+  // for the aligned, contiguous case (the generic plan covers the rest)
+  Problem p{};
+  p.x = reinterpret_cast<const void*>(uintptr_t(256));
+  p.row_stride = n;
+  p.dtype = dtype;
+  p.m = m; p.n = n; p.k = k; p.b = b; p.kb = kb;
+  p.layout = layout;
+  p.geo = geo_for(dtype, n);
+  return std::max(plan_generic(m, n, k, b, kb).total(), fused_workspace_bytes(p));
 }
 
 int btk_uses_fused_path(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, int dtype,
@@ -174,7 +181,11 @@ int btk_approx_topk(const void* x, int64_t row_stride, int dtype, int64_t m, int
   p.layout = layout;
   p.geo = geo_for(dtype, n);
   p.flag = flag;
-  if (fused_supported(p)) return cuda_status(run_fused(p, out_vals, out_idx, st));
+  if (fused_supported(p)) {
+    const size_t need = fused_workspace_bytes(p);
+    if (ws_bytes < need || (need && (reinterpret_cast<uintptr_t>(ws) & 255))) return BTK_ERR_WORKSPACE;
+    return cuda_status(run_fused(p, out_vals, out_idx, ws, ws_bytes, st));
+  }
 
   const Plan pl = plan_generic(m, n, k, b, kb);
   if (ws_bytes < pl.total() || (pl.total() && (reinterpret_cast<uintptr_t>(ws) & 255)))

@@ -48,7 +48,18 @@ namespace cg = cooperative_groups;
 
 namespace btk {
 
+// Development timeline trace (BTK_TRACE=1): per CTA, globaltimer at start,
+// first stage landed, streaming done, merged, end, ranked, SM id.  Read
+// with btk_trace_read(); never enabled in production runs.
+__device__ unsigned long long g_trace[8192][8];
+
 namespace {
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 constexpr int WIDE_NT = 512;
 constexpr int WIDE_U = 8;                  // 16-byte loads in flight per thread
@@ -280,7 +291,7 @@ __device__ __forceinline__ RankSmem rank_smem(uint64_t* pool, uint8_t* aux, int 
 template <int DT, int NT, int ITEMS>
 __device__ __forceinline__ void stage2_emit(uint64_t* pool, uint8_t* aux, int64_t P, int64_t k,
                                             int lognb, int64_t row, const CompGeo& geo,
-                                            void* out_vals, int64_t* out_idx) {
+                                            void* out_vals, int64_t* out_idx, bool trace_on = false) {
   if constexpr (ITEMS == 0) {
     for (int64_t p = P + threadIdx.x; p < 64; p += NT) pool[p] = 0ull;
     __syncthreads();
@@ -293,6 +304,7 @@ __device__ __forceinline__ void stage2_emit(uint64_t* pool, uint8_t* aux, int64_
   else {
     const RankSmem S = rank_smem(pool, aux, (int)k, lognb, NT);
     rank_select_sort<DT, NT, ITEMS>(S, (int)P, (int)k, lognb, geo.ib);
+    if (trace_on && threadIdx.x == 0 && blockIdx.x < 8192) g_trace[blockIdx.x][5] = gtime();
     pdl_wait_writes();
     for (int64_t q = threadIdx.x; q < k; q += NT)
       emit_comp<DT>(rs_key(pool, S.inv[q]), row * k + q, geo, out_vals, out_idx);
@@ -478,6 +490,7 @@ struct NarrowArgs {
   void* out_vals;
   int64_t* out_idx;
   uint32_t* flag;
+  int trace;
 };
 
 template <int DT, int KB, int NT, int ITEMS>
@@ -489,6 +502,8 @@ __global__ void __launch_bounds__(NT) fused_narrow(NarrowArgs a) {
 
   cg::cluster_group cluster = cg::this_cluster();
   const int crank = (int)cluster.block_rank();
+  const bool tr = a.trace && threadIdx.x == 0 && blockIdx.x < 8192;
+  if (tr) g_trace[blockIdx.x][0] = gtime();
   const int64_t row = blockIdx.x / a.S;
   const int tid = threadIdx.x;
   const int64_t b = a.b, s = a.s;
@@ -538,6 +553,7 @@ __global__ void __launch_bounds__(NT) fused_narrow(NarrowArgs a) {
   for (int i = 0; i < nstages; ++i) {
     const int slot = i % a.NS;
     mbar_wait(&full[slot], (uint32_t)((i / a.NS) & 1));
+    if (tr && i == 0) g_trace[blockIdx.x][1] = gtime();
     const int64_t t0 = t_begin + (int64_t)i * a.T;
     const int rows = (int)min((int64_t)a.T, t_end - t0);
     // the ragged final view-row (only partially valid) is handled last
@@ -559,6 +575,7 @@ __global__ void __launch_bounds__(NT) fused_narrow(NarrowArgs a) {
     if (tid == 0 && i + a.NS < nstages) issue(i + a.NS);
   }
   const uint32_t bad = sc.nonfinite() ? 1u : 0u;
+  if (tr) g_trace[blockIdx.x][2] = gtime();
 
   // ---- phase queues -> smem (the ring is dead now)
   uint64_t* scratch = reinterpret_cast<uint64_t*>(smem + a.scratch_off);
@@ -598,10 +615,368 @@ __global__ void __launch_bounds__(NT) fused_narrow(NarrowArgs a) {
     }
   }
   if (a.S > 1) cluster.sync();  // remote partials stay alive until read
-  if (crank != 0) return;
+  if (tr) g_trace[blockIdx.x][3] = gtime();
+  if (crank != 0) {
+    if (tr) g_trace[blockIdx.x][4] = gtime();
+    return;
+  }
   __syncthreads();
+  if (tr) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_trace[blockIdx.x][6] = smid;
+  }
   stage2_emit<DT, NT, ITEMS>(pool, smem + a.aux_off, a.P, a.k, a.lognb, row, a.geo, a.out_vals,
-                            a.out_idx);
+                            a.out_idx, a.trace != 0);
+  if (tr) g_trace[blockIdx.x][4] = gtime();
+}
+
+// ============================================================ split (TMA ring, persistent)
+// Work-balanced form of the narrow kernel for few, long rows (cfg1): the m
+// rows are flattened into m*s view-rows and CTA c of C (a multiple of the
+// SM count) streams the contiguous share [c*M/C, (c+1)*M/C) through its TMA
+// ring, so every SM reads the same number of bytes regardless of how rows
+// fall.  A share is cut into row segments; at each segment end the CTA
+// folds its phase queues into a per-bucket partial.  A row covered by one
+// CTA goes straight to Stage 2; otherwise each covering CTA publishes its
+// partial (global workspace, L2-resident), and the LAST to arrive on the
+// row's counter merges them and runs Stage 2 (threadfence-reduction
+// pattern: no spinning, no inter-CTA waits).  Counters are reset by the
+// merging CTA, so the workspace stays zero between calls.
+struct SplitArgs {
+  const void* x;
+  int64_t row_stride;
+  int64_t m, n, k, b, kb, s;
+  int G, R, T, NS, C;
+  int sort_items, lognb;
+  int64_t P;
+  size_t stage_bytes;
+  size_t scratch_off, part_off, pool_off, aux_off;
+  uint64_t* part_ws;   // C x 2 x (b*KB) comps (slot 0: first row of the share, 1: last)
+  uint32_t* counters;  // m arrival counters (zero between calls)
+  int kbs;             // KB of the instance (part stride)
+  CompGeo geo;
+  void* out_vals;
+  int64_t* out_idx;
+  uint32_t* flag;
+};
+
+__device__ __forceinline__ int64_t split_cta_of(int64_t v, int64_t M, int C) {
+  return ((v + 1) * (int64_t)C - 1) / M;  // largest c with c*M/C <= v
+}
+
+template <int DT, int KB, int NT, int ITEMS>
+__global__ void __launch_bounds__(NT) fused_split(SplitArgs a) {
+  constexpr int V = Vec<DT>::V;
+  constexpr int ESZ = VT<DT>::W / 8;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[MAX_STAGES];
+  __shared__ int s_last;
+
+  const int tid = threadIdx.x;
+  const int64_t b = a.b, s = a.s;
+  const int64_t M = a.m * s;
+  const int c = blockIdx.x;
+  const int64_t v0 = ((int64_t)c * M) / a.C, v1 = ((int64_t)(c + 1) * M) / a.C;
+  if (v0 >= v1) return;
+  const uint8_t* xb = static_cast<const uint8_t*>(a.x);
+
+  if (tid == 0) {
+    for (int i = 0; i < a.NS; ++i) mbar_init(&full[i], 1);
+    fence_barrier_init();
+  }
+  pdl_trigger();
+  pdl_wait();
+  __syncthreads();
+
+  // producer cursor (thread 0): stages never straddle a row boundary
+  int64_t pv = v0;
+  int issued = 0;
+  uint64_t policy = 0;
+  auto issue = [&]() {
+    const int slot = issued % a.NS;
+    const int64_t row = pv / s;
+    const int64_t len = min((int64_t)a.T, min((row + 1) * s, v1) - pv);
+    const uint32_t bytes = (uint32_t)(len * b * ESZ);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&full[slot], bytes);
+    bulk_g2s(smem + (size_t)slot * a.stage_bytes,
+             xb + (row * a.row_stride + (pv - row * s) * b) * ESZ, bytes, &full[slot], policy);
+    pv += len;
+    ++issued;
+  };
+  if (tid == 0) {
+    policy = evict_first_policy();
+    for (int i = 0; i < a.NS && pv < v1; ++i) issue();
+  }
+
+  const int G = a.G, R = a.R;
+  const int r = tid / G, g = tid - r * G;
+  const bool active = r < R;
+  Scanner<DT, KB> sc;
+  sc.init();
+  const uint32_t smem_base = smem_u32(smem) + (uint32_t)(g * V * ESZ);
+  const uint32_t row_step = (uint32_t)(R * b * ESZ);
+  uint64_t* scratch = reinterpret_cast<uint64_t*>(smem + a.scratch_off);
+  uint64_t* part = reinterpret_cast<uint64_t*>(smem + a.part_off);
+  uint64_t* pool = reinterpret_cast<uint64_t*>(smem + a.pool_off);
+  uint32_t bad = 0;
+  const int64_t P = a.P;
+  const int64_t first_row = v0 / s;
+
+  int64_t v = v0;
+  for (int i = 0; v < v1; ++i) {
+    const int slot = i % a.NS;
+    const int64_t row = v / s;
+    const int64_t tin = v - row * s;  // view-row within the row
+    const int len = (int)min((int64_t)a.T, min((row + 1) * s, v1) - v);
+    mbar_wait(&full[slot], (uint32_t)((i / a.NS) & 1));
+    if (active) {
+      uint32_t addr = smem_base + (uint32_t)(slot * a.stage_bytes) + (uint32_t)(r * b * ESZ);
+#pragma unroll 4
+      for (int rr = r; rr < len; rr += R) {
+        sc.row(lds128(addr), (int)(tin + rr));
+        addr += row_step;
+      }
+    }
+    __syncthreads();  // slot consumed by every thread
+    if (tid == 0 && pv < v1) issue();
+    v += len;
+    if (v != (row + 1) * s && v != v1) continue;
+
+    // ---- segment end: fold the phase queues into the row's partial
+    bad |= sc.nonfinite() ? 1u : 0u;
+    if (active) sc.template spill<KB>(scratch + (int64_t)r * b * KB, g, b, 0, a.geo);
+    sc.init();
+    __syncthreads();
+    for (int64_t j = tid; j < b; j += NT) {
+      uint64_t best[KB];
+#pragma unroll
+      for (int z = 0; z < KB; ++z) best[z] = 0ull;
+      for (int rr = 0; rr < R; ++rr) {
+#pragma unroll
+        for (int z = 0; z < KB; ++z) comp_push<KB>(best, scratch[((int64_t)rr * b + j) * KB + z]);
+      }
+#pragma unroll
+      for (int z = 0; z < KB; ++z) part[j * KB + z] = best[z];
+    }
+    const int64_t cfirst = split_cta_of(row * s, M, a.C), clast = split_cta_of((row + 1) * s - 1, M, a.C);
+    bool mine = true;
+    if (cfirst != clast) {
+      // publish, then count arrivals; the last one merges
+      uint64_t* dst = a.part_ws + ((int64_t)c * 2 + (row == first_row ? 0 : 1)) * b * KB;
+      __syncthreads();
+      for (int64_t j = tid; j < b * KB; j += NT) dst[j] = part[j];
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) {
+        const uint32_t old = atomicAdd(&a.counters[row], 1u);
+        s_last = (old == (uint32_t)(clast - cfirst)) ? 1 : 0;
+      }
+      __syncthreads();
+      mine = s_last != 0;
+      if (mine) {
+        __threadfence();
+        for (int64_t j = tid; j < b; j += NT) {
+          uint64_t best[KB];
+#pragma unroll
+          for (int z = 0; z < KB; ++z) best[z] = 0ull;
+          for (int64_t cc = cfirst; cc <= clast; ++cc) {
+            const int64_t w = ((cc * M) / a.C) / s == row ? 0 : 1;
+            const uint64_t* src = a.part_ws + (cc * 2 + w) * b * KB + j * KB;
+#pragma unroll
+            for (int z = 0; z < KB; ++z) comp_push<KB>(best, __ldcg(src + z));
+          }
+#pragma unroll
+          for (int z = 0; z < KB; ++z) part[j * KB + z] = best[z];
+        }
+        if (tid == 0) a.counters[row] = 0u;
+      }
+    }
+    if (mine) {
+      __syncthreads();
+      for (int64_t j = tid; j < b; j += NT) {
+#pragma unroll
+        for (int z = 0; z < KB; ++z)
+          if (z < a.kb) pool[j * a.kb + z] = part[j * KB + z];
+      }
+      __syncthreads();
+      stage2_emit<DT, NT, ITEMS>(pool, smem + a.aux_off, P, a.k, a.lognb, row, a.geo, a.out_vals,
+                                 a.out_idx);
+    }
+    __syncthreads();  // scratch / part / pool reused by the next segment
+  }
+  if (__syncthreads_or(bad) && tid == 0 && a.flag) atomicOr(a.flag, 1u);
+}
+
+// ============================================================ rows (one warp per row)
+// Many short rows (cfg4: 4096 x 32768, b = 512): block-level barriers and
+// a CTA-wide sort per row would serialise the tail of every row.  Here a
+// WARP owns a row end to end: lane l streams vector columns l, l+32, ...
+// (GPL per lane) with U 128-bit loads in flight per column, keeps the
+// register queues, spills its b*k_b survivors to a per-warp shared pool,
+// and runs a warp-synchronous version of the bucketing/rank engine
+// (btk_rank.cuh) — only __syncwarp, so the 32 warps of an SM progress
+// independently and one warp's tail overlaps the others' streaming.
+struct RowsArgs {
+  const void* x;
+  int64_t row_stride;
+  int64_t m, n, k, b, kb, s;
+  int G, last_vec, lognb;
+  int64_t P;
+  size_t warp_smem, inv_off, hist_off;
+  CompGeo geo;
+  void* out_vals;
+  int64_t* out_idx;
+  uint32_t* flag;
+};
+
+template <int DT, int ITEMS>
+__device__ __forceinline__ void warp_rank_sort(uint64_t* pool, int P, int k, uint16_t* inv,
+                                               uint32_t* hist, int lognb, int ib) {
+  const int lane = threadIdx.x & 31;
+  for (int q = lane; q < k; q += 32) inv[q] = RS_NONE;
+  uint64_t key[ITEMS];
+  uint32_t slot[ITEMS];
+  uint64_t mn = ~0ull, mx = 0ull;
+  float vmn = __int_as_float(0x7F800000), vmx = -__int_as_float(0x7F800000);
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int p = lane + 32 * i;
+    key[i] = p < P ? pool[p] : 0ull;
+    if (key[i]) {
+      mn = key[i] < mn ? key[i] : mn;
+      mx = key[i] > mx ? key[i] : mx;
+      const float v = comp_value<DT>(key[i], ib);
+      vmn = fminf(vmn, v);
+      vmx = fmaxf(vmx, v);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const uint64_t a = __shfl_xor_sync(0xFFFFFFFFu, mn, o);
+    const uint64_t b = __shfl_xor_sync(0xFFFFFFFFu, mx, o);
+    mn = a < mn ? a : mn;
+    mx = b > mx ? b : mx;
+    vmn = fminf(vmn, __shfl_xor_sync(0xFFFFFFFFu, vmn, o));
+    vmx = fmaxf(vmx, __shfl_xor_sync(0xFFFFFFFFu, vmx, o));
+  }
+  if (mx == 0ull) { __syncwarp(); return; }
+  RsRule R;
+  R.nb = 1 << lognb;
+  R.mn = mn;
+  R.vmx = vmx;
+  R.same = (mn == mx);
+  R.shift = max(0, bits64(mx - mn) - lognb);
+  const float span = vmx - vmn;
+  R.scale = (float)R.nb / span;
+  const bool narrow_band = (vmn > 0.f && vmx < 4.f * vmn) || (vmx < 0.f && vmn > 4.f * vmx);
+  R.vmode = !narrow_band && (span > 0.f) && (R.scale > 0.f) && (R.scale < 3.0e38f) &&
+            (span < 3.0e38f);
+  for (int j = lane; j < R.nb + 2; j += 32) hist[j] = 0u;
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i)
+    if (lane + 32 * i < P) slot[i] = atomicAdd(&hist[rs_bucket<DT>(R, key[i], ib)], 1u);
+  __syncwarp();
+  {  // warp exclusive scan of hist[0 .. nb+2)
+    const int len = R.nb + 2, chunk = (len + 31) / 32, b0 = lane * chunk;
+    uint32_t sum = 0;
+    for (int i = 0; i < chunk; ++i) sum += (b0 + i < len) ? hist[b0 + i] : 0u;
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    uint32_t run = incl - sum;
+    __syncwarp();
+    for (int i = 0; i < chunk; ++i) {
+      if (b0 + i < len) {
+        const uint32_t c = hist[b0 + i];
+        hist[b0 + i] = run;
+        run += c;
+      }
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i)
+    if (lane + 32 * i < P) pool[hist[rs_bucket<DT>(R, key[i], ib)] + slot[i]] = key[i];
+  __syncwarp();
+  for (int p = lane; p < P; p += 32) {
+    const uint64_t x = pool[p];
+    if (!x) continue;
+    if (R.same) {
+      if (p < k) inv[p] = (uint16_t)p;
+      continue;
+    }
+    const int d = rs_bucket<DT>(R, x, ib);
+    const int s0 = (int)hist[d], s1 = (int)hist[d + 1];
+    if (s0 >= k) continue;
+    int cnt = 0;
+    for (int j = s0; j < s1; ++j) {
+      const uint64_t y = pool[j];
+      cnt += (y > x || (y == x && j < p)) ? 1 : 0;
+    }
+    const int f = s0 + cnt;
+    if (f < k) inv[f] = (uint16_t)p;
+  }
+  __syncwarp();
+}
+
+template <int DT, int KB, int GPL, int U, int ITEMS>
+__global__ void __launch_bounds__(256) fused_rows(RowsArgs a) {
+  constexpr int V = Vec<DT>::V;
+  constexpr int ESZ = VT<DT>::W / 8;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* wsm = smem + (size_t)warp * a.warp_smem;
+  uint64_t* pool = reinterpret_cast<uint64_t*>(wsm);
+  uint16_t* inv = reinterpret_cast<uint16_t*>(wsm + a.inv_off);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(wsm + a.hist_off);
+  const int64_t b = a.b, s = a.s;
+  const int G = a.G;
+  uint32_t bad = 0;
+  pdl_trigger();
+  pdl_wait();
+  for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < a.m; row += (int64_t)gridDim.x * 8) {
+    const uint8_t* rowp = static_cast<const uint8_t*>(a.x) + row * a.row_stride * ESZ;
+    Scanner<DT, KB> sc[GPL];
+#pragma unroll
+    for (int j = 0; j < GPL; ++j) sc[j].init();
+#pragma unroll
+    for (int j = 0; j < GPL; ++j) {
+      const int g = lane + 32 * j;
+      if (g < G) {
+        const uint8_t* colp = rowp + (int64_t)g * V * ESZ;
+        const int64_t s_eff = (g < a.last_vec) ? s : s - 1;
+        int64_t t0 = 0;
+        for (; t0 + U <= s_eff; t0 += U) {
+          uint4 v[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) v[u] = ldg_stream(colp + (t0 + u) * b * ESZ);
+#pragma unroll
+          for (int u = 0; u < U; ++u) sc[j].row(v[u], (int)(t0 + u));
+        }
+        for (; t0 < s_eff; ++t0) sc[j].row(ldg_stream(colp + t0 * b * ESZ), (int)t0);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < GPL; ++j) {
+      const int g = lane + 32 * j;
+      if (g < G) {
+        bad |= sc[j].nonfinite() ? 1u : 0u;
+        sc[j].template spill<KB>(pool, g, b, 0, a.geo);
+      }
+    }
+    __syncwarp();
+    warp_rank_sort<DT, ITEMS>(pool, (int)a.P, (int)a.k, inv, hist, a.lognb, a.geo.ib);
+    for (int64_t q = lane; q < a.k; q += 32)
+      emit_comp<DT>(rs_key(pool, inv[q]), row * a.k + q, a.geo, a.out_vals, a.out_idx);
+    __syncwarp();
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0 && a.flag) atomicOr(a.flag, 1u);
 }
 
 // ============================================================ wide (LDG, one CTA per row)
@@ -672,15 +1047,31 @@ __global__ void __launch_bounds__(NT, 1) fused_wide(WideArgs a) {
 }
 
 // ============================================================ planning
-enum Kind { NONE = 0, NARROW = 1, WIDE = 2 };
+enum Kind { NONE = 0, NARROW = 1, WIDE = 2, SPLIT = 3, ROWS = 4 };
 
 struct Plan {
   Kind kind = NONE;
   int nt = 0;
   size_t smem = 0;
+  size_t ws = 0;  // device workspace (split kernel: partials + row counters)
   NarrowArgs na{};
   WideArgs wa{};
+  SplitArgs sa{};
+  RowsArgs ra{};
+  int rows_gpl = 0, rows_items = 0;
 };
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+      v = NUM_SMS;
+    n = v;
+  }
+  return n;
+}
 
 bool common_envelope(const Problem& p) {
   if (p.layout != 0 || p.kb > 8) return false;
@@ -703,12 +1094,6 @@ bool plan_narrow(const Problem& p, Plan& pl) {
   a.G = (int)G;
   a.R = (int)(NT / G);
   const int64_t vrow_bytes = p.b * esz;
-  // stage: ~16 KB of whole view-rows, a multiple of R rows when possible
-  int64_t T = std::max<int64_t>(1, ((int64_t)env_int("BTK_STAGE_KB", 16) * 1024) / vrow_bytes);
-  if (T >= a.R) T = (T / a.R) * a.R;
-  if (T * vrow_bytes > 64 * 1024) return false;
-  a.T = (int)T;
-  a.stage_bytes = (size_t)(T * vrow_bytes);
   a.last_vec = (int)((p.n - (s - 1) * p.b) / V);
   a.P = P;
   a.sort_items = sort_items_for(P, NT);
@@ -722,31 +1107,36 @@ bool plan_narrow(const Problem& p, Plan& pl) {
   a.pool_off = regA + a16((size_t)p.b * kbt * 8);
   a.aux_off = a.pool_off + (P <= 64 ? 64 * 8 : a16((size_t)P * 8));
   const size_t post = a.pool_off + stage2_bytes(P, p.k, NT);
-  // cluster size: split rows until the grid fills one resident wave
+  // Launch shape (measured on B200, tools/sweep_narrow2.sh): rows of >= 1 MB
+  // run one CTA per row with a deep ring (3 x 48 KB in flight; cfg3 94% of
+  // the copy peak); shorter rows split over a cluster of S CTAs so about
+  // two CTAs land per SM, each with >= 64 KB (cfg1: S = 2, 2 x 32 KB).
   const int64_t row_bytes = p.n * esz;
+  const int nsm = num_sms();
   int S = 1;
-  int NS = 1;
+  if (row_bytes < (1 << 20)) {
+    while (S < 8 && p.m * (S * 2) <= 2 * (int64_t)nsm && row_bytes / (S * 2) >= 64 * 1024) S *= 2;
+  }
+  if (env_int("BTK_S", 0)) S = env_int("BTK_S", 0);
+  while (S < 8 && (s + S - 1) / S >= 0xFFFF) S *= 2;  // 16-bit slot codes of the packed scanner
+  if (S > s || (s + S - 1) / S >= 0xFFFF) return false;
+  const bool deep = row_bytes / S >= (1 << 20);
+  int NS = env_int("BTK_NS", deep ? 3 : 2);
+  int stage_kb = env_int("BTK_STAGE_KB", deep ? 48 : 32);
   size_t smem = 0;
-  const int force_s = env_int("BTK_S", 0);
-  for (int cand = 8; cand >= 1; cand >>= 1) {
-    if (cand > s) continue;
-    if (force_s && cand != force_s) continue;
-    const int64_t range_rows = (s + cand - 1) / cand;
-    if (range_rows >= 0xFFFF) continue;  // 16-bit slot codes of the packed scanner
-    const int64_t stages = (range_rows + T - 1) / T;
-    const int ns = (int)std::min<int64_t>(std::min<int64_t>(stages, env_int("BTK_NS", 2)), MAX_STAGES);
-    const size_t sm = std::max(post, (size_t)ns * a.stage_bytes);
-    const int per_sm_smem = (int)(SMEM_LIMIT / (sm + 1024));
-    const int per_sm = std::min(per_sm_smem, 2048 / NT);
-    if (per_sm < 1) continue;
-    const int64_t slots = (int64_t)per_sm * NUM_SMS;
-    if (p.m * cand <= slots || cand == 1) {
-      // prefer the largest split that still fits one wave when rows are few
-      if (p.m * cand <= slots && (row_bytes / cand) >= 16 * 1024) {
-        S = cand; NS = ns; smem = sm;
-        break;
-      }
-      if (cand == 1 || force_s) { S = cand; NS = ns; smem = sm; }
+  for (;; stage_kb /= 2) {
+    int64_t T = std::max<int64_t>(1, ((int64_t)stage_kb * 1024) / vrow_bytes);
+    if (T >= a.R) T = (T / a.R) * a.R;
+    if (T * vrow_bytes > 64 * 1024) return false;
+    const int64_t stages = ((s + S - 1) / S + T - 1) / T;
+    const int ns = (int)std::min<int64_t>(std::min<int64_t>(stages, NS), MAX_STAGES);
+    const size_t sm = std::max(post, (size_t)ns * (size_t)(T * vrow_bytes));
+    if (sm <= SMEM_LIMIT || stage_kb <= 8) {
+      a.T = (int)T;
+      a.stage_bytes = (size_t)(T * vrow_bytes);
+      NS = ns;
+      smem = sm;
+      break;
     }
   }
   if (smem == 0 || smem > SMEM_LIMIT) return false;
@@ -754,6 +1144,7 @@ bool plan_narrow(const Problem& p, Plan& pl) {
   a.NS = NS;
   a.geo = p.geo;
   a.flag = p.flag;
+  a.trace = env_int("BTK_TRACE", 0);
   pl.kind = NARROW;
   pl.nt = NT;
   pl.smem = smem;
@@ -782,8 +1173,86 @@ bool plan_wide(const Problem& p, Plan& pl) {
   return pl.smem <= SMEM_LIMIT;
 }
 
+// Persistent work-balanced variant (fused_split): b | n, whole view-rows.
+bool plan_split(const Problem& p, Plan& pl) {
+  const int V = vec_of(p.dtype), esz = esz_of(p.dtype);
+  if (p.n % p.b) return false;
+  const int64_t G = p.b / V, s = p.n / p.b, P = p.b * p.kb;
+  const int NT = G <= 16 ? 128 : 256;
+  if (G > NT || s >= 0xFFFF) return false;
+  SplitArgs& a = pl.sa;
+  a.x = p.x; a.row_stride = p.row_stride;
+  a.m = p.m; a.n = p.n; a.k = p.k; a.b = p.b; a.kb = p.kb; a.s = s;
+  a.G = (int)G;
+  a.R = (int)(NT / G);
+  const int64_t vrow_bytes = p.b * esz;
+  int64_t T = std::max<int64_t>(1, ((int64_t)env_int("BTK_STAGE_KB", 16) * 1024) / vrow_bytes);
+  if (T >= a.R) T = (T / a.R) * a.R;
+  if (T * vrow_bytes > 64 * 1024) return false;
+  a.T = (int)T;
+  a.stage_bytes = (size_t)(T * vrow_bytes);
+  a.P = P;
+  a.sort_items = sort_items_for(P, NT);
+  if (a.sort_items > 32) return false;
+  a.lognb = rank_lognb(P);
+  const int kbt = kb_tmpl(p.kb);
+  a.kbs = kbt;
+  a.NS = std::min(env_int("BTK_NS", 4), MAX_STAGES);
+  a.scratch_off = a16((size_t)a.NS * a.stage_bytes);
+  a.part_off = a.scratch_off + a16((size_t)a.R * p.b * kbt * 8);
+  a.pool_off = a.part_off + a16((size_t)p.b * kbt * 8);
+  a.aux_off = a.pool_off + (P <= 64 ? 64 * 8 : a16((size_t)P * 8));
+  const size_t smem = a.pool_off + stage2_bytes(P, p.k, NT);
+  if (smem > SMEM_LIMIT) return false;
+  const int per_sm_smem = (int)(SMEM_LIMIT / (smem + 1024));
+  const int cps = std::max(1, std::min({per_sm_smem, 2048 / NT, env_int("BTK_CPS", 4)}));
+  const int64_t M = p.m * s;
+  a.C = (int)std::min<int64_t>((int64_t)num_sms() * cps, M);
+  a.geo = p.geo;
+  a.flag = p.flag;
+  pl.kind = SPLIT;
+  pl.nt = NT;
+  pl.smem = smem;
+  pl.ws = a16((size_t)a.C * 2 * p.b * kbt * 8) + a16((size_t)p.m * 4);
+  return true;
+}
+
+// One warp per row (fused_rows): many rows, b <= 64 vectors, pool <= 1024.
+bool plan_rows(const Problem& p, Plan& pl) {
+  const int V = vec_of(p.dtype);
+  const int64_t G = p.b / V, s = (p.n + p.b - 1) / p.b, P = p.b * p.kb;
+  if (p.kb != kb_tmpl(p.kb) || G > 64 || P > 1024 || s >= 0xFFFF) return false;
+  RowsArgs& a = pl.ra;
+  a.x = p.x; a.row_stride = p.row_stride;
+  a.m = p.m; a.n = p.n; a.k = p.k; a.b = p.b; a.kb = p.kb; a.s = s;
+  a.G = (int)G;
+  a.last_vec = (int)((p.n - (s - 1) * p.b) / V);
+  a.P = P;
+  a.lognb = std::min(rank_lognb(P), 8);
+  a.inv_off = a16((size_t)std::max<int64_t>(P, 32) * 8);
+  a.hist_off = a.inv_off + a16((size_t)p.k * 2);
+  a.warp_smem = a.hist_off + a16((size_t)((1 << a.lognb) + 2) * 4);
+  const size_t smem = 8 * a.warp_smem;
+  if (smem > SMEM_LIMIT) return false;
+  pl.rows_gpl = G <= 32 ? 1 : 2;
+  pl.rows_items = P <= 256 ? 8 : (P <= 512 ? 16 : 32);
+  a.geo = p.geo;
+  a.flag = p.flag;
+  pl.kind = ROWS;
+  pl.nt = 256;
+  pl.smem = smem;
+  return true;
+}
+
 bool make_plan(const Problem& p, Plan& pl) {
   if (!common_envelope(p)) return false;
+  const int want_rows = env_int("BTK_ROWS", -1);
+  const bool rows = want_rows >= 0 ? want_rows != 0 : p.m >= 8 * (int64_t)num_sms();
+  if (rows && plan_rows(p, pl)) return true;
+  // few long rows: balance bytes over SMs (split); many rows: one row per CTA
+  const int want_split = env_int("BTK_SPLIT", -1);
+  const bool split = want_split > 0;  // opt-in (BTK_SPLIT=1): measured slower than the cluster kernel on cfg1/cfg3
+  if (split && plan_split(p, pl)) return true;
   if (plan_narrow(p, pl)) return true;
   return plan_wide(p, pl);
 }
@@ -843,7 +1312,65 @@ cudaError_t launch_wide(const Plan& pl, cudaStream_t st) {
 }
 
 template <int DT, int KB>
+cudaError_t launch_split(const Plan& pl, cudaStream_t st) {
+  const SplitArgs& a = pl.sa;
+  void (*kern)(SplitArgs);
+  switch (a.sort_items) {
+    case 0: kern = pl.nt == 128 ? fused_split<DT, KB, 128, 0> : fused_split<DT, KB, 256, 0>; break;
+    case 2: kern = pl.nt == 128 ? fused_split<DT, KB, 128, 2> : fused_split<DT, KB, 256, 2>; break;
+    case 8: kern = pl.nt == 128 ? fused_split<DT, KB, 128, 8> : fused_split<DT, KB, 256, 8>; break;
+    default: kern = pl.nt == 128 ? fused_split<DT, KB, 128, 32> : fused_split<DT, KB, 256, 32>; break;
+  }
+  cudaError_t e = ensure_smem_attr((const void*)kern, pl.smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)a.C);
+  cfg.blockDim = dim3(pl.nt);
+  cfg.dynamicSmemBytes = pl.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+template <int DT, int KB, int GPL, int ITEMS>
+cudaError_t launch_rows_t(const Plan& pl, cudaStream_t st) {
+  constexpr int U = GPL == 1 ? 8 : 4;
+  auto kern = fused_rows<DT, KB, GPL, U, ITEMS>;
+  cudaError_t e = ensure_smem_attr((const void*)kern, pl.smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, pl.nt, pl.smem);
+  if (e != cudaSuccess) return e;
+  const int64_t want = (pl.ra.m + 7) / 8;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)std::max(1, per_sm) * num_sms()));
+  kern<<<grid, pl.nt, pl.smem, st>>>(pl.ra);
+  return cudaGetLastError();
+}
+
+template <int DT, int KB>
+cudaError_t launch_rows(const Plan& pl, cudaStream_t st) {
+  if constexpr (VT<DT>::W == 32 && KB == 8) {
+    return cudaErrorNotSupported;  // 4 x 8 queue entries per column: register budget
+  } else {
+    if (pl.rows_gpl == 1) {
+      if (pl.rows_items == 8) return launch_rows_t<DT, KB, 1, 8>(pl, st);
+      if (pl.rows_items == 16) return launch_rows_t<DT, KB, 1, 16>(pl, st);
+      return launch_rows_t<DT, KB, 1, 32>(pl, st);
+    }
+    if (pl.rows_items == 8) return launch_rows_t<DT, KB, 2, 8>(pl, st);
+    if (pl.rows_items == 16) return launch_rows_t<DT, KB, 2, 16>(pl, st);
+    return launch_rows_t<DT, KB, 2, 32>(pl, st);
+  }
+}
+
+template <int DT, int KB>
 cudaError_t launch_any(const Plan& pl, cudaStream_t st) {
+  if (pl.kind == ROWS) return launch_rows<DT, KB>(pl, st);
+  if (pl.kind == SPLIT) return launch_split<DT, KB>(pl, st);
   return pl.kind == NARROW ? launch_narrow<DT, KB>(pl, st) : launch_wide<DT, KB>(pl, st);
 }
 
@@ -863,11 +1390,24 @@ bool fused_supported(const Problem& p) {
   return make_plan(p, pl);
 }
 
-cudaError_t run_fused(const Problem& p, void* out_vals, int64_t* out_idx, cudaStream_t st) {
+size_t fused_workspace_bytes(const Problem& p) {
+  Plan pl;
+  return make_plan(p, pl) ? pl.ws : 0;
+}
+
+cudaError_t run_fused(const Problem& p, void* out_vals, int64_t* out_idx, void* ws, size_t ws_bytes,
+                      cudaStream_t st) {
   Plan pl;
   if (!make_plan(p, pl)) return cudaErrorNotSupported;
-  pl.na.out_vals = pl.wa.out_vals = out_vals;
-  pl.na.out_idx = pl.wa.out_idx = out_idx;
+  if (ws_bytes < pl.ws || (pl.ws && (reinterpret_cast<uintptr_t>(ws) & 255)))
+    return cudaErrorInvalidValue;
+  pl.na.out_vals = pl.wa.out_vals = pl.sa.out_vals = pl.ra.out_vals = out_vals;
+  pl.na.out_idx = pl.wa.out_idx = pl.sa.out_idx = pl.ra.out_idx = out_idx;
+  if (pl.kind == SPLIT) {
+    uint8_t* w = static_cast<uint8_t*>(ws);
+    pl.sa.part_ws = reinterpret_cast<uint64_t*>(w);
+    pl.sa.counters = reinterpret_cast<uint32_t*>(w + a16((size_t)pl.sa.C * 2 * p.b * pl.sa.kbs * 8));
+  }
   cudaError_t e = cudaErrorInvalidValue;
   switch (p.dtype) {
     case F32: e = launch_kb<F32>(pl, p.kb, st); break;
@@ -882,3 +1422,8 @@ cudaError_t run_fused(const Problem& p, void* out_vals, int64_t* out_idx, cudaSt
 }
 
 }  // namespace btk
+
+extern "C" int btk_trace_read(void* host_dst, int nblocks) {
+  if (nblocks > 8192) nblocks = 8192;
+  return (int)cudaMemcpyFromSymbol(host_dst, btk::g_trace, (size_t)nblocks * 8 * 8);
+}

@@ -72,7 +72,11 @@ cudaError_t run_stage1_emit(const Problem& p, const uint64_t* pool, int64_t C, v
                             int64_t* out_idx, cudaStream_t st);
 // Fused interleaved fast path (stage 1 + stage 2 in one kernel per row group).
 // Returns cudaErrorNotSupported when the shape is outside its envelope.
-cudaError_t run_fused(const Problem& p, void* out_vals, int64_t* out_idx, cudaStream_t st);
+// ws: fused_workspace_bytes(p) bytes, 256-aligned, zero-filled before first
+// use (the split kernel's row counters; every call leaves them zero).
+cudaError_t run_fused(const Problem& p, void* out_vals, int64_t* out_idx, void* ws, size_t ws_bytes,
+                      cudaStream_t st);
 bool fused_supported(const Problem& p);
+size_t fused_workspace_bytes(const Problem& p);
 
 }  // namespace btk
