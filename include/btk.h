@@ -70,11 +70,8 @@ int btk_stage1_validate(int64_t n, int64_t b, int64_t kb);
  * reference core.py:155-158 (stage1_candidate_count). */
 int64_t btk_stage1_count(int64_t n, int64_t b, int64_t kb, int layout);
 
-/* Bytes of device workspace btk_approx_topk needs (0 is possible).  The
- * workspace must be zero-filled before its FIRST use with a given problem
- * shape; every call leaves it zero-filled again (it carries per-row arrival
- * counters of the work-balanced kernel), so it can be reused across calls
- * on the same stream without re-clearing. */
+/* Bytes of device workspace btk_approx_topk needs (0 is possible; the
+ * fused kernels need none).  Contents need not be initialised. */
 size_t btk_workspace_bytes(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, int dtype,
                            int layout);
 

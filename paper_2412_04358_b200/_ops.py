@@ -88,10 +88,9 @@ def as_rows(t: torch.Tensor, dim: int = -1):
 
 
 def workspace(nbytes: int, device) -> torch.Tensor:
-    """Zero-filled device workspace (include/btk.h: zero before first use;
-    the library leaves it zero).  torch's caching allocator returns
-    >= 512-byte aligned blocks."""
-    return torch.zeros(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+    """Device workspace (contents need not be initialised).  torch's
+    caching allocator returns >= 512-byte aligned blocks."""
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
 
 
 def stream_handle(device) -> int:

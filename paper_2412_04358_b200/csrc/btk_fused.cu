@@ -631,184 +631,6 @@ __global__ void __launch_bounds__(NT) fused_narrow(NarrowArgs a) {
   if (tr) g_trace[blockIdx.x][4] = gtime();
 }
 
-// ============================================================ split (TMA ring, persistent)
-// Work-balanced form of the narrow kernel for few, long rows (cfg1): the m
-// rows are flattened into m*s view-rows and CTA c of C (a multiple of the
-// SM count) streams the contiguous share [c*M/C, (c+1)*M/C) through its TMA
-// ring, so every SM reads the same number of bytes regardless of how rows
-// fall.  A share is cut into row segments; at each segment end the CTA
-// folds its phase queues into a per-bucket partial.  A row covered by one
-// CTA goes straight to Stage 2; otherwise each covering CTA publishes its
-// partial (global workspace, L2-resident), and the LAST to arrive on the
-// row's counter merges them and runs Stage 2 (threadfence-reduction
-// pattern: no spinning, no inter-CTA waits).  Counters are reset by the
-// merging CTA, so the workspace stays zero between calls.
-struct SplitArgs {
-  const void* x;
-  int64_t row_stride;
-  int64_t m, n, k, b, kb, s;
-  int G, R, T, NS, C;
-  int sort_items, lognb;
-  int64_t P;
-  size_t stage_bytes;
-  size_t scratch_off, part_off, pool_off, aux_off;
-  uint64_t* part_ws;   // C x 2 x (b*KB) comps (slot 0: first row of the share, 1: last)
-  uint32_t* counters;  // m arrival counters (zero between calls)
-  int kbs;             // KB of the instance (part stride)
-  CompGeo geo;
-  void* out_vals;
-  int64_t* out_idx;
-  uint32_t* flag;
-};
-
-__device__ __forceinline__ int64_t split_cta_of(int64_t v, int64_t M, int C) {
-  return ((v + 1) * (int64_t)C - 1) / M;  // largest c with c*M/C <= v
-}
-
-template <int DT, int KB, int NT, int ITEMS>
-__global__ void __launch_bounds__(NT) fused_split(SplitArgs a) {
-  constexpr int V = Vec<DT>::V;
-  constexpr int ESZ = VT<DT>::W / 8;
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[MAX_STAGES];
-  __shared__ int s_last;
-
-  const int tid = threadIdx.x;
-  const int64_t b = a.b, s = a.s;
-  const int64_t M = a.m * s;
-  const int c = blockIdx.x;
-  const int64_t v0 = ((int64_t)c * M) / a.C, v1 = ((int64_t)(c + 1) * M) / a.C;
-  if (v0 >= v1) return;
-  const uint8_t* xb = static_cast<const uint8_t*>(a.x);
-
-  if (tid == 0) {
-    for (int i = 0; i < a.NS; ++i) mbar_init(&full[i], 1);
-    fence_barrier_init();
-  }
-  pdl_trigger();
-  pdl_wait();
-  __syncthreads();
-
-  // producer cursor (thread 0): stages never straddle a row boundary
-  int64_t pv = v0;
-  int issued = 0;
-  uint64_t policy = 0;
-  auto issue = [&]() {
-    const int slot = issued % a.NS;
-    const int64_t row = pv / s;
-    const int64_t len = min((int64_t)a.T, min((row + 1) * s, v1) - pv);
-    const uint32_t bytes = (uint32_t)(len * b * ESZ);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(&full[slot], bytes);
-    bulk_g2s(smem + (size_t)slot * a.stage_bytes,
-             xb + (row * a.row_stride + (pv - row * s) * b) * ESZ, bytes, &full[slot], policy);
-    pv += len;
-    ++issued;
-  };
-  if (tid == 0) {
-    policy = evict_first_policy();
-    for (int i = 0; i < a.NS && pv < v1; ++i) issue();
-  }
-
-  const int G = a.G, R = a.R;
-  const int r = tid / G, g = tid - r * G;
-  const bool active = r < R;
-  Scanner<DT, KB> sc;
-  sc.init();
-  const uint32_t smem_base = smem_u32(smem) + (uint32_t)(g * V * ESZ);
-  const uint32_t row_step = (uint32_t)(R * b * ESZ);
-  uint64_t* scratch = reinterpret_cast<uint64_t*>(smem + a.scratch_off);
-  uint64_t* part = reinterpret_cast<uint64_t*>(smem + a.part_off);
-  uint64_t* pool = reinterpret_cast<uint64_t*>(smem + a.pool_off);
-  uint32_t bad = 0;
-  const int64_t P = a.P;
-  const int64_t first_row = v0 / s;
-
-  int64_t v = v0;
-  for (int i = 0; v < v1; ++i) {
-    const int slot = i % a.NS;
-    const int64_t row = v / s;
-    const int64_t tin = v - row * s;  // view-row within the row
-    const int len = (int)min((int64_t)a.T, min((row + 1) * s, v1) - v);
-    mbar_wait(&full[slot], (uint32_t)((i / a.NS) & 1));
-    if (active) {
-      uint32_t addr = smem_base + (uint32_t)(slot * a.stage_bytes) + (uint32_t)(r * b * ESZ);
-#pragma unroll 4
-      for (int rr = r; rr < len; rr += R) {
-        sc.row(lds128(addr), (int)(tin + rr));
-        addr += row_step;
-      }
-    }
-    __syncthreads();  // slot consumed by every thread
-    if (tid == 0 && pv < v1) issue();
-    v += len;
-    if (v != (row + 1) * s && v != v1) continue;
-
-    // ---- segment end: fold the phase queues into the row's partial
-    bad |= sc.nonfinite() ? 1u : 0u;
-    if (active) sc.template spill<KB>(scratch + (int64_t)r * b * KB, g, b, 0, a.geo);
-    sc.init();
-    __syncthreads();
-    for (int64_t j = tid; j < b; j += NT) {
-      uint64_t best[KB];
-#pragma unroll
-      for (int z = 0; z < KB; ++z) best[z] = 0ull;
-      for (int rr = 0; rr < R; ++rr) {
-#pragma unroll
-        for (int z = 0; z < KB; ++z) comp_push<KB>(best, scratch[((int64_t)rr * b + j) * KB + z]);
-      }
-#pragma unroll
-      for (int z = 0; z < KB; ++z) part[j * KB + z] = best[z];
-    }
-    const int64_t cfirst = split_cta_of(row * s, M, a.C), clast = split_cta_of((row + 1) * s - 1, M, a.C);
-    bool mine = true;
-    if (cfirst != clast) {
-      // publish, then count arrivals; the last one merges
-      uint64_t* dst = a.part_ws + ((int64_t)c * 2 + (row == first_row ? 0 : 1)) * b * KB;
-      __syncthreads();
-      for (int64_t j = tid; j < b * KB; j += NT) dst[j] = part[j];
-      __threadfence();
-      __syncthreads();
-      if (tid == 0) {
-        const uint32_t old = atomicAdd(&a.counters[row], 1u);
-        s_last = (old == (uint32_t)(clast - cfirst)) ? 1 : 0;
-      }
-      __syncthreads();
-      mine = s_last != 0;
-      if (mine) {
-        __threadfence();
-        for (int64_t j = tid; j < b; j += NT) {
-          uint64_t best[KB];
-#pragma unroll
-          for (int z = 0; z < KB; ++z) best[z] = 0ull;
-          for (int64_t cc = cfirst; cc <= clast; ++cc) {
-            const int64_t w = ((cc * M) / a.C) / s == row ? 0 : 1;
-            const uint64_t* src = a.part_ws + (cc * 2 + w) * b * KB + j * KB;
-#pragma unroll
-            for (int z = 0; z < KB; ++z) comp_push<KB>(best, __ldcg(src + z));
-          }
-#pragma unroll
-          for (int z = 0; z < KB; ++z) part[j * KB + z] = best[z];
-        }
-        if (tid == 0) a.counters[row] = 0u;
-      }
-    }
-    if (mine) {
-      __syncthreads();
-      for (int64_t j = tid; j < b; j += NT) {
-#pragma unroll
-        for (int z = 0; z < KB; ++z)
-          if (z < a.kb) pool[j * a.kb + z] = part[j * KB + z];
-      }
-      __syncthreads();
-      stage2_emit<DT, NT, ITEMS>(pool, smem + a.aux_off, P, a.k, a.lognb, row, a.geo, a.out_vals,
-                                 a.out_idx);
-    }
-    __syncthreads();  // scratch / part / pool reused by the next segment
-  }
-  if (__syncthreads_or(bad) && tid == 0 && a.flag) atomicOr(a.flag, 1u);
-}
-
 // ============================================================ rows (one warp per row)
 // Many short rows (cfg4: 4096 x 32768, b = 512): block-level barriers and
 // a CTA-wide sort per row would serialise the tail of every row.  Here a
@@ -1047,16 +869,15 @@ __global__ void __launch_bounds__(NT, 1) fused_wide(WideArgs a) {
 }
 
 // ============================================================ planning
-enum Kind { NONE = 0, NARROW = 1, WIDE = 2, SPLIT = 3, ROWS = 4 };
+enum Kind { NONE = 0, NARROW = 1, WIDE = 2, ROWS = 3 };
 
 struct Plan {
   Kind kind = NONE;
   int nt = 0;
   size_t smem = 0;
-  size_t ws = 0;  // device workspace (split kernel: partials + row counters)
+  size_t ws = 0;  // device workspace (none of the fused kernels needs one today)
   NarrowArgs na{};
   WideArgs wa{};
-  SplitArgs sa{};
   RowsArgs ra{};
   int rows_gpl = 0, rows_items = 0;
 };
@@ -1173,50 +994,6 @@ bool plan_wide(const Problem& p, Plan& pl) {
   return pl.smem <= SMEM_LIMIT;
 }
 
-// Persistent work-balanced variant (fused_split): b | n, whole view-rows.
-bool plan_split(const Problem& p, Plan& pl) {
-  const int V = vec_of(p.dtype), esz = esz_of(p.dtype);
-  if (p.n % p.b) return false;
-  const int64_t G = p.b / V, s = p.n / p.b, P = p.b * p.kb;
-  const int NT = G <= 16 ? 128 : 256;
-  if (G > NT || s >= 0xFFFF) return false;
-  SplitArgs& a = pl.sa;
-  a.x = p.x; a.row_stride = p.row_stride;
-  a.m = p.m; a.n = p.n; a.k = p.k; a.b = p.b; a.kb = p.kb; a.s = s;
-  a.G = (int)G;
-  a.R = (int)(NT / G);
-  const int64_t vrow_bytes = p.b * esz;
-  int64_t T = std::max<int64_t>(1, ((int64_t)env_int("BTK_STAGE_KB", 16) * 1024) / vrow_bytes);
-  if (T >= a.R) T = (T / a.R) * a.R;
-  if (T * vrow_bytes > 64 * 1024) return false;
-  a.T = (int)T;
-  a.stage_bytes = (size_t)(T * vrow_bytes);
-  a.P = P;
-  a.sort_items = sort_items_for(P, NT);
-  if (a.sort_items > 32) return false;
-  a.lognb = rank_lognb(P);
-  const int kbt = kb_tmpl(p.kb);
-  a.kbs = kbt;
-  a.NS = std::min(env_int("BTK_NS", 4), MAX_STAGES);
-  a.scratch_off = a16((size_t)a.NS * a.stage_bytes);
-  a.part_off = a.scratch_off + a16((size_t)a.R * p.b * kbt * 8);
-  a.pool_off = a.part_off + a16((size_t)p.b * kbt * 8);
-  a.aux_off = a.pool_off + (P <= 64 ? 64 * 8 : a16((size_t)P * 8));
-  const size_t smem = a.pool_off + stage2_bytes(P, p.k, NT);
-  if (smem > SMEM_LIMIT) return false;
-  const int per_sm_smem = (int)(SMEM_LIMIT / (smem + 1024));
-  const int cps = std::max(1, std::min({per_sm_smem, 2048 / NT, env_int("BTK_CPS", 4)}));
-  const int64_t M = p.m * s;
-  a.C = (int)std::min<int64_t>((int64_t)num_sms() * cps, M);
-  a.geo = p.geo;
-  a.flag = p.flag;
-  pl.kind = SPLIT;
-  pl.nt = NT;
-  pl.smem = smem;
-  pl.ws = a16((size_t)a.C * 2 * p.b * kbt * 8) + a16((size_t)p.m * 4);
-  return true;
-}
-
 // One warp per row (fused_rows): many rows, b <= 64 vectors, pool <= 1024.
 bool plan_rows(const Problem& p, Plan& pl) {
   const int V = vec_of(p.dtype);
@@ -1249,10 +1026,6 @@ bool make_plan(const Problem& p, Plan& pl) {
   const int want_rows = env_int("BTK_ROWS", -1);
   const bool rows = want_rows >= 0 ? want_rows != 0 : p.m >= 8 * (int64_t)num_sms();
   if (rows && plan_rows(p, pl)) return true;
-  // few long rows: balance bytes over SMs (split); many rows: one row per CTA
-  const int want_split = env_int("BTK_SPLIT", -1);
-  const bool split = want_split > 0;  // opt-in (BTK_SPLIT=1): measured slower than the cluster kernel on cfg1/cfg3
-  if (split && plan_split(p, pl)) return true;
   if (plan_narrow(p, pl)) return true;
   return plan_wide(p, pl);
 }
@@ -1311,31 +1084,6 @@ cudaError_t launch_wide(const Plan& pl, cudaStream_t st) {
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-template <int DT, int KB>
-cudaError_t launch_split(const Plan& pl, cudaStream_t st) {
-  const SplitArgs& a = pl.sa;
-  void (*kern)(SplitArgs);
-  switch (a.sort_items) {
-    case 0: kern = pl.nt == 128 ? fused_split<DT, KB, 128, 0> : fused_split<DT, KB, 256, 0>; break;
-    case 2: kern = pl.nt == 128 ? fused_split<DT, KB, 128, 2> : fused_split<DT, KB, 256, 2>; break;
-    case 8: kern = pl.nt == 128 ? fused_split<DT, KB, 128, 8> : fused_split<DT, KB, 256, 8>; break;
-    default: kern = pl.nt == 128 ? fused_split<DT, KB, 128, 32> : fused_split<DT, KB, 256, 32>; break;
-  }
-  cudaError_t e = ensure_smem_attr((const void*)kern, pl.smem);
-  if (e != cudaSuccess) return e;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)a.C);
-  cfg.blockDim = dim3(pl.nt);
-  cfg.dynamicSmemBytes = pl.smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, a);
-}
-
 template <int DT, int KB, int GPL, int ITEMS>
 cudaError_t launch_rows_t(const Plan& pl, cudaStream_t st) {
   constexpr int U = GPL == 1 ? 8 : 4;
@@ -1370,7 +1118,6 @@ cudaError_t launch_rows(const Plan& pl, cudaStream_t st) {
 template <int DT, int KB>
 cudaError_t launch_any(const Plan& pl, cudaStream_t st) {
   if (pl.kind == ROWS) return launch_rows<DT, KB>(pl, st);
-  if (pl.kind == SPLIT) return launch_split<DT, KB>(pl, st);
   return pl.kind == NARROW ? launch_narrow<DT, KB>(pl, st) : launch_wide<DT, KB>(pl, st);
 }
 
@@ -1401,13 +1148,9 @@ cudaError_t run_fused(const Problem& p, void* out_vals, int64_t* out_idx, void* 
   if (!make_plan(p, pl)) return cudaErrorNotSupported;
   if (ws_bytes < pl.ws || (pl.ws && (reinterpret_cast<uintptr_t>(ws) & 255)))
     return cudaErrorInvalidValue;
-  pl.na.out_vals = pl.wa.out_vals = pl.sa.out_vals = pl.ra.out_vals = out_vals;
-  pl.na.out_idx = pl.wa.out_idx = pl.sa.out_idx = pl.ra.out_idx = out_idx;
-  if (pl.kind == SPLIT) {
-    uint8_t* w = static_cast<uint8_t*>(ws);
-    pl.sa.part_ws = reinterpret_cast<uint64_t*>(w);
-    pl.sa.counters = reinterpret_cast<uint32_t*>(w + a16((size_t)pl.sa.C * 2 * p.b * pl.sa.kbs * 8));
-  }
+  pl.na.out_vals = pl.wa.out_vals = pl.ra.out_vals = out_vals;
+  pl.na.out_idx = pl.wa.out_idx = pl.ra.out_idx = out_idx;
+
   cudaError_t e = cudaErrorInvalidValue;
   switch (p.dtype) {
     case F32: e = launch_kb<F32>(pl, p.kb, st); break;
