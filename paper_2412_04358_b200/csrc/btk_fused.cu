@@ -999,6 +999,7 @@ bool plan_rows(const Problem& p, Plan& pl) {
   const int V = vec_of(p.dtype);
   const int64_t G = p.b / V, s = (p.n + p.b - 1) / p.b, P = p.b * p.kb;
   if (p.kb != kb_tmpl(p.kb) || G > 64 || P > 1024 || s >= 0xFFFF) return false;
+  if (V * p.kb > 16) return false;  // register queues per lane (see launch_rows)
   RowsArgs& a = pl.ra;
   a.x = p.x; a.row_stride = p.row_stride;
   a.m = p.m; a.n = p.n; a.k = p.k; a.b = p.b; a.kb = p.kb; a.s = s;
@@ -1101,8 +1102,8 @@ cudaError_t launch_rows_t(const Plan& pl, cudaStream_t st) {
 
 template <int DT, int KB>
 cudaError_t launch_rows(const Plan& pl, cudaStream_t st) {
-  if constexpr (VT<DT>::W == 32 && KB == 8) {
-    return cudaErrorNotSupported;  // 4 x 8 queue entries per column: register budget
+  if constexpr (Vec<DT>::V * KB > 16) {
+    return cudaErrorNotSupported;  // plan_rows never selects these (register budget)
   } else {
     if (pl.rows_gpl == 1) {
       if (pl.rows_items == 8) return launch_rows_t<DT, KB, 1, 8>(pl, st);

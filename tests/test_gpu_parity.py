@@ -234,3 +234,29 @@ def test_sharded_equals_single():
     devs = ["cuda:0"] * 3  # same device three times: exercises the partition logic
     r = btk.approx_topk_sharded(x, 256, sch, devices=devs)
     assert torch.equal(r.indices, base.indices) and torch.equal(r.values, base.values)
+
+
+_SHAPE_ENVS = [{"BTK_ROWS": "1"}, {"BTK_ROWS": "0", "BTK_S": "1"}, {"BTK_ROWS": "0", "BTK_S": "2"},
+               {"BTK_ROWS": "0", "BTK_S": "4"}, {"BTK_ROWS": "0", "BTK_S": "8"},
+               {"BTK_ROWS": "0", "BTK_S": "2", "BTK_STAGE_KB": "8", "BTK_NS": "3"}]
+
+
+@pytest.mark.parametrize("env", _SHAPE_ENVS, ids=lambda e: "-".join(f"{k[4:]}{v}" for k, v in e.items()))
+def test_fused_launch_shapes_match_oracle(env, monkeypatch):
+    """Every fused kernel / cluster split / ring shape gives the oracle's
+    bits (results must not depend on the launch shape: reference
+    approx.py:8-16 mode-independence, test_approx.py:194-207)."""
+    for k_, v_ in env.items():
+        monkeypatch.setenv(k_, v_)
+    rng = np.random.default_rng(77)
+    cases = [(3, 65536, 64, 64, 1), (2, 32768, 512, 512, 1), (2, 20000, 300, 256, 2),
+             (3, 40000, 512, 128, 4), (2, 33000, 256, 64, 8), (4, 8192 + 64, 100, 64, 2),
+             (2, 131072, 256, 1024, 1), (3, 4096, 64, 16, 4)]
+    for m, n, k, b, kb in cases:
+        for kind in ("normal", "ties"):
+            x32 = _rand_input(rng, kind, m, n)
+            wv, wi = O.approx_topk(x32, k, b, kb)
+            for dn in _dtypes_for(x32):
+                x = torch.from_numpy(x32).to(DT[dn]).cuda()
+                r = btk.approx_topk(x, k, btk.BucketScheme(b, kb, I))
+                assert_same(r, wv, wi, DT[dn])
