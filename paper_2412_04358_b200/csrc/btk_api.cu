@@ -68,6 +68,7 @@ struct Carve {
 
 // Stage 1 into the bucket-major pool (m x b*kb comps).
 int stage1_pool(const Problem& p, const Plan& pl, Carve& cv, uint64_t* pool, cudaStream_t st) {
+  if (stage1_vec_supported(p)) return cuda_status(run_stage1_vec(p, pool, st));
   if (p.kb <= 16) return cuda_status(run_stage1_generic(p, pool, st));
   uint64_t* mat = cv.take(pl.mat);
   uint64_t* s1a = cv.take(pl.s1a);

@@ -273,20 +273,6 @@ __device__ __forceinline__ void warp_sort64_desc(uint64_t* sk) {
 // write of the first k.  `aux` is the engine's shared-memory scratch
 // (rank_aux_bytes).  ITEMS is exact per kernel instance so the register
 // budget of small-pool kernels is not set by the largest pools.
-__device__ __forceinline__ RankSmem rank_smem(uint64_t* pool, uint8_t* aux, int k, int lognb, int nt) {
-  RankSmem S;
-  S.pool = pool;
-  S.hist = reinterpret_cast<uint32_t*>(aux);
-  aux += ((size_t)((1 << lognb) + 2) * 4 + 127) / 128 * 128;
-  S.inv = reinterpret_cast<uint16_t*>(aux);
-  aux += ((size_t)k * 2 + 127) / 128 * 128;
-  S.work = reinterpret_cast<int2*>(aux);
-  aux += (size_t)RS_WORK * 8;
-  S.red = reinterpret_cast<uint64_t*>(aux);
-  aux += (size_t)(nt / 32) * 24;
-  S.ctl = reinterpret_cast<int*>(aux);
-  return S;
-}
 
 template <int DT, int NT, int ITEMS>
 __device__ __forceinline__ void stage2_emit(uint64_t* pool, uint8_t* aux, int64_t P, int64_t k,
@@ -302,7 +288,7 @@ __device__ __forceinline__ void stage2_emit(uint64_t* pool, uint8_t* aux, int64_
     return;
   }
   else {
-    const RankSmem S = rank_smem(pool, aux, (int)k, lognb, NT);
+    const RankSmem S = rank_smem(pool, aux, P, k, lognb, NT);
     rank_select_sort<DT, NT, ITEMS>(S, (int)P, (int)k, lognb, geo.ib);
     if (trace_on && threadIdx.x == 0 && blockIdx.x < 8192) g_trace[blockIdx.x][5] = gtime();
     pdl_wait_writes();
@@ -324,7 +310,7 @@ int sort_items_for(int64_t P, int NT) {
 // Stage-2 shared memory after the pool's P keys.
 size_t stage2_bytes(int64_t P, int64_t k, int NT) {
   if (P <= 64) return 64 * 8;
-  return ((size_t)P * 8 + 127) / 128 * 128 + rank_aux_bytes(NT, rank_lognb(P), k);
+  return ((size_t)P * 8 + 127) / 128 * 128 + rank_aux_bytes(NT, rank_lognb(P), k, P);
 }
 size_t a16(size_t v) { return (v + 127) & ~(size_t)127; }
 
@@ -646,7 +632,7 @@ struct RowsArgs {
   int64_t m, n, k, b, kb, s;
   int G, last_vec, lognb;
   int64_t P;
-  size_t warp_smem, inv_off, hist_off;
+  size_t warp_smem, inv_off, hist_off, bid_off;
   CompGeo geo;
   void* out_vals;
   int64_t* out_idx;
@@ -655,7 +641,7 @@ struct RowsArgs {
 
 template <int DT, int ITEMS>
 __device__ __forceinline__ void warp_rank_sort(uint64_t* pool, int P, int k, uint16_t* inv,
-                                               uint32_t* hist, int lognb, int ib) {
+                                               uint16_t* bid, uint32_t* hist, int lognb, int ib) {
   const int lane = threadIdx.x & 31;
   for (int q = lane; q < k; q += 32) inv[q] = RS_NONE;
   uint64_t key[ITEMS];
@@ -697,9 +683,14 @@ __device__ __forceinline__ void warp_rank_sort(uint64_t* pool, int P, int k, uin
             (span < 3.0e38f);
   for (int j = lane; j < R.nb + 2; j += 32) hist[j] = 0u;
   __syncwarp();
+  uint16_t dd[ITEMS];
 #pragma unroll
-  for (int i = 0; i < ITEMS; ++i)
-    if (lane + 32 * i < P) slot[i] = atomicAdd(&hist[rs_bucket<DT>(R, key[i], ib)], 1u);
+  for (int i = 0; i < ITEMS; ++i) {
+    if (lane + 32 * i < P) {
+      dd[i] = (uint16_t)rs_bucket<DT>(R, key[i], ib);
+      slot[i] = atomicAdd(&hist[dd[i]], 1u);
+    }
+  }
   __syncwarp();
   {  // warp exclusive scan of hist[0 .. nb+2)
     const int len = R.nb + 2, chunk = (len + 31) / 32, b0 = lane * chunk;
@@ -723,8 +714,13 @@ __device__ __forceinline__ void warp_rank_sort(uint64_t* pool, int P, int k, uin
   }
   __syncwarp();
 #pragma unroll
-  for (int i = 0; i < ITEMS; ++i)
-    if (lane + 32 * i < P) pool[hist[rs_bucket<DT>(R, key[i], ib)] + slot[i]] = key[i];
+  for (int i = 0; i < ITEMS; ++i) {
+    if (lane + 32 * i < P) {
+      const int q = (int)hist[dd[i]] + (int)slot[i];
+      pool[q] = key[i];
+      bid[q] = dd[i];
+    }
+  }
   __syncwarp();
   for (int p = lane; p < P; p += 32) {
     const uint64_t x = pool[p];
@@ -733,7 +729,7 @@ __device__ __forceinline__ void warp_rank_sort(uint64_t* pool, int P, int k, uin
       if (p < k) inv[p] = (uint16_t)p;
       continue;
     }
-    const int d = rs_bucket<DT>(R, x, ib);
+    const int d = bid[p];
     const int s0 = (int)hist[d], s1 = (int)hist[d + 1];
     if (s0 >= k) continue;
     int cnt = 0;
@@ -757,6 +753,7 @@ __global__ void __launch_bounds__(256) fused_rows(RowsArgs a) {
   uint64_t* pool = reinterpret_cast<uint64_t*>(wsm);
   uint16_t* inv = reinterpret_cast<uint16_t*>(wsm + a.inv_off);
   uint32_t* hist = reinterpret_cast<uint32_t*>(wsm + a.hist_off);
+  uint16_t* bid = reinterpret_cast<uint16_t*>(wsm + a.bid_off);
   const int64_t b = a.b, s = a.s;
   const int G = a.G;
   uint32_t bad = 0;
@@ -793,7 +790,7 @@ __global__ void __launch_bounds__(256) fused_rows(RowsArgs a) {
       }
     }
     __syncwarp();
-    warp_rank_sort<DT, ITEMS>(pool, (int)a.P, (int)a.k, inv, hist, a.lognb, a.geo.ib);
+    warp_rank_sort<DT, ITEMS>(pool, (int)a.P, (int)a.k, inv, bid, hist, a.lognb, a.geo.ib);
     for (int64_t q = lane; q < a.k; q += 32)
       emit_comp<DT>(rs_key(pool, inv[q]), row * a.k + q, a.geo, a.out_vals, a.out_idx);
     __syncwarp();
@@ -815,6 +812,7 @@ struct WideArgs {
   void* out_vals;
   int64_t* out_idx;
   uint32_t* flag;
+  int trace;
 };
 
 template <int DT, int KB, int NT, int U, int ITEMS>
@@ -830,6 +828,8 @@ __global__ void __launch_bounds__(NT, 1) fused_wide(WideArgs a) {
   uint32_t bad = 0;
   pdl_trigger();
   pdl_wait();
+  const bool tr = a.trace && tid == 0 && blockIdx.x < 8192;
+  if (tr) g_trace[blockIdx.x][0] = gtime();
   for (int64_t g = tid; g < a.G; g += NT) {
     Queue<KB> q[V];
 #pragma unroll
@@ -863,9 +863,48 @@ __global__ void __launch_bounds__(NT, 1) fused_wide(WideArgs a) {
         if (z < a.kb) pool[col * a.kb + z] = comp_of<DT>(q[e].v[z], q[e].t[z], col, b, a.geo);
     }
   }
+  if (tr) g_trace[blockIdx.x][2] = g_trace[blockIdx.x][3] = gtime();
   if (__syncthreads_or(nonfinite_hit<DT>(bad)) && tid == 0 && a.flag) atomicOr(a.flag, 1u);
   stage2_emit<DT, NT, ITEMS>(pool, smem + a.aux_off, a.P, a.k, a.lognb, row, a.geo, a.out_vals,
-                            a.out_idx);
+                            a.out_idx, a.trace != 0);
+  if (tr) g_trace[blockIdx.x][4] = gtime();
+}
+
+// ============================================================ stage-1 pool (vector columns)
+// Stage 1 alone for the generic (pool in global memory) path when the pool
+// is too large for one CTA (cfg5: b = 65536, k_b = 2 -> 131072 survivors
+// per row).  Same per-thread vector-column scan as fused_wide, but one
+// thread per column across the whole grid and all of a column's slots in
+// flight at once; survivors go to pool[row][j*k_b + z] (btk_stage1.cu's
+// layout), the input to K2.
+template <int DT, int KB, int U>
+__global__ void __launch_bounds__(256) s1_vec(const void* __restrict__ x, int64_t row_stride,
+                                              int64_t n, int64_t b, int64_t s, int64_t G,
+                                              int last_vec, CompGeo geo,
+                                              uint64_t* __restrict__ pool, uint32_t* flag) {
+  constexpr int V = Vec<DT>::V;
+  constexpr int ESZ = VT<DT>::W / 8;
+  const int64_t row = blockIdx.y;
+  const int64_t g = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  uint32_t bad = 0;
+  if (g < G) {
+    const uint8_t* colp = static_cast<const uint8_t*>(x) + (row * row_stride + g * V) * ESZ;
+    const int64_t s_eff = (g < last_vec) ? s : s - 1;
+    Scanner<DT, KB> sc;
+    sc.init();
+    int64_t t0 = 0;
+    for (; t0 + U <= s_eff; t0 += U) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = ldg_stream(colp + (t0 + u) * b * ESZ);
+#pragma unroll
+      for (int u = 0; u < U; ++u) sc.row(v[u], (int)(t0 + u));
+    }
+    for (; t0 < s_eff; ++t0) sc.row(ldg_stream(colp + t0 * b * ESZ), (int)t0);
+    bad = sc.nonfinite() ? 1u : 0u;
+    sc.template spill<KB>(pool + row * b * KB, (int)g, b, 0, geo);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0 && flag) atomicOr(flag, 1u);
 }
 
 // ============================================================ planning
@@ -988,6 +1027,7 @@ bool plan_wide(const Problem& p, Plan& pl) {
   a.aux_off = P <= 64 ? 64 * 8 : a16((size_t)P * 8);
   a.geo = p.geo;
   a.flag = p.flag;
+  a.trace = env_int("BTK_TRACE", 0);
   pl.smem = stage2_bytes(P, p.k, WIDE_NT);
   pl.kind = WIDE;
   pl.nt = WIDE_NT;
@@ -1009,7 +1049,8 @@ bool plan_rows(const Problem& p, Plan& pl) {
   a.lognb = std::min(rank_lognb(P), 8);
   a.inv_off = a16((size_t)std::max<int64_t>(P, 32) * 8);
   a.hist_off = a.inv_off + a16((size_t)p.k * 2);
-  a.warp_smem = a.hist_off + a16((size_t)((1 << a.lognb) + 2) * 4);
+  a.bid_off = a.hist_off + a16((size_t)((1 << a.lognb) + 2) * 4);
+  a.warp_smem = a.bid_off + a16((size_t)std::max<int64_t>(P, 32) * 2);
   const size_t smem = 8 * a.warp_smem;
   if (smem > SMEM_LIMIT) return false;
   pl.rows_gpl = G <= 32 ? 1 : 2;
@@ -1136,6 +1177,47 @@ cudaError_t launch_kb(const Plan& pl, int64_t kb, cudaStream_t st) {
 bool fused_supported(const Problem& p) {
   Plan pl;
   return make_plan(p, pl);
+}
+
+bool stage1_vec_supported(const Problem& p) {
+  const int V = vec_of(p.dtype), esz = esz_of(p.dtype);
+  if (p.layout != 0 || p.kb != kb_tmpl(p.kb) || V * p.kb > 16) return false;
+  if (p.b % V || p.n % V) return false;
+  if ((reinterpret_cast<uintptr_t>(p.x) & 15) || ((p.row_stride * esz) & 15)) return false;
+  const int64_t s = (p.n + p.b - 1) / p.b;
+  return s < 0xFFFF && p.m <= 65535;
+}
+
+template <int DT, int KB>
+static cudaError_t launch_s1_vec(const Problem& p, uint64_t* pool, cudaStream_t st) {
+  constexpr int V = Vec<DT>::V;
+  const int64_t G = p.b / V, s = (p.n + p.b - 1) / p.b;
+  const int last_vec = (int)((p.n - (s - 1) * p.b) / V);
+  dim3 grid((unsigned)((G + 255) / 256), (unsigned)p.m);
+  if (s <= 16) s1_vec<DT, KB, 16><<<grid, 256, 0, st>>>(p.x, p.row_stride, p.n, p.b, s, G, last_vec, p.geo, pool, p.flag);
+  else s1_vec<DT, KB, 8><<<grid, 256, 0, st>>>(p.x, p.row_stride, p.n, p.b, s, G, last_vec, p.geo, pool, p.flag);
+  return cudaGetLastError();
+}
+
+template <int DT>
+static cudaError_t s1_vec_dt(const Problem& p, uint64_t* pool, cudaStream_t st) {
+  switch (p.kb) {
+    case 1: return launch_s1_vec<DT, 1>(p, pool, st);
+    case 2: return launch_s1_vec<DT, 2>(p, pool, st);
+    case 4: return launch_s1_vec<DT, 4>(p, pool, st);
+  }
+  if constexpr (Vec<DT>::V * 8 <= 16) return launch_s1_vec<DT, 8>(p, pool, st);
+  return cudaErrorNotSupported;
+}
+
+cudaError_t run_stage1_vec(const Problem& p, uint64_t* pool, cudaStream_t st) {
+  if (!stage1_vec_supported(p)) return cudaErrorNotSupported;
+  switch (p.dtype) {
+    case F32: return s1_vec_dt<F32>(p, pool, st);
+    case BF16: return s1_vec_dt<BF16>(p, pool, st);
+    case F16: return s1_vec_dt<F16>(p, pool, st);
+  }
+  return cudaErrorInvalidValue;
 }
 
 size_t fused_workspace_bytes(const Problem& p) {

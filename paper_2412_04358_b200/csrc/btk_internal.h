@@ -65,6 +65,10 @@ struct Problem {
 // Generic stage 1, k_b <= 16: one thread per (row, bucket), register queue.
 // pool: m x (b*kb) comps, bucket-major, sorted within bucket, 0 = empty.
 cudaError_t run_stage1_generic(const Problem& p, uint64_t* pool, cudaStream_t st);
+// Vectorised stage 1 into the same pool (interleaved, k_b in {1,2,4,8},
+// V*k_b <= 16, 16-byte aligned rows); cudaErrorNotSupported otherwise.
+bool stage1_vec_supported(const Problem& p);
+cudaError_t run_stage1_vec(const Problem& p, uint64_t* pool, cudaStream_t st);
 // All of a row's elements as comps, bucket-major (m*b segments of s slots).
 cudaError_t run_materialize(const Problem& p, uint64_t* mat, cudaStream_t st);
 // pool (m x b*kb) -> compact (m x C) values/indices in bucket order.

@@ -46,6 +46,7 @@ __device__ __forceinline__ uint64_t rs_key(const uint64_t* pool, uint16_t pos) {
 struct RankSmem {
   uint64_t* pool;   // P keys (permuted in place)
   uint16_t* inv;    // >= k entries
+  uint16_t* bid;    // P entries: bucket of each pool position (current level)
   uint32_t* hist;   // (1 << lognb) + 2 counters
   int2* work;       // RS_WORK ranges
   uint64_t* red;    // 3 * (NT / 32) words of scratch
@@ -188,17 +189,25 @@ __device__ __forceinline__ void rs_range(const RankSmem& S, int lo, int hi, int 
   const bool narrow_band = (vmn > 0.f && vmx < 4.f * vmn) || (vmx < 0.f && vmn > 4.f * vmx);
   R.vmode = !narrow_band && (span > 0.f) && (R.scale > 0.f) && (R.scale < 3.0e38f) &&
             (span < 3.0e38f);
+  uint16_t dd[ITEMS];
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const int p = tid + i * NT;
-    if (p < n) slot[i] = atomicAdd(&S.hist[rs_bucket<DT>(R, key[i], ib)], 1u);
+    if (p < n) {
+      dd[i] = (uint16_t)rs_bucket<DT>(R, key[i], ib);
+      slot[i] = atomicAdd(&S.hist[dd[i]], 1u);
+    }
   }
   __syncthreads();
   block_exscan<NT>(S.hist, R.nb + 2, reinterpret_cast<uint32_t*>(S.red));
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const int p = tid + i * NT;
-    if (p < n) S.pool[lo + S.hist[rs_bucket<DT>(R, key[i], ib)] + slot[i]] = key[i];
+    if (p < n) {
+      const int q = lo + (int)S.hist[dd[i]] + (int)slot[i];
+      S.pool[q] = key[i];
+      S.bid[q] = dd[i];
+    }
   }
   __syncthreads();
   // rank pass over positions in bucket order
@@ -209,7 +218,7 @@ __device__ __forceinline__ void rs_range(const RankSmem& S, int lo, int hi, int 
       if (lo + p < k) S.inv[lo + p] = (uint16_t)(lo + p);
       continue;
     }
-    const int d = rs_bucket<DT>(R, x, ib);
+    const int d = S.bid[lo + p];
     const int s0 = (int)S.hist[d], s1 = (int)S.hist[d + 1];
     if (lo + s0 >= k) continue;  // bucket lies wholly beyond the k-th key
     if (s1 - s0 > RS_LIMIT) {
@@ -250,17 +259,38 @@ __device__ void rank_select_sort(const RankSmem& S, int P, int k, int lognb, int
   __syncthreads();
 }
 
-// Shared-memory bytes the engine needs besides the pool.
-__host__ __device__ constexpr size_t rank_aux_bytes(int nt, int lognb, int64_t k) {
+// Shared-memory bytes the engine needs besides the pool (P keys).
+__host__ __device__ constexpr size_t rank_aux_bytes(int nt, int lognb, int64_t k, int64_t P) {
   return ((size_t)((1 << lognb) + 2) * 4 + 127) / 128 * 128 +  // hist
          ((size_t)k * 2 + 127) / 128 * 128 +                   // inv
+         ((size_t)P * 2 + 127) / 128 * 128 +                   // bid
          (size_t)RS_WORK * 8 + (size_t)(nt / 32) * 24 + 128;  // work, red, ctl
 }
 
-// Choose log2(#buckets) for a pool of P keys: ~4 keys per bucket, 256..4096.
+// Carve the engine's scratch out of `aux` (rank_aux_bytes of it).
+__device__ __forceinline__ RankSmem rank_smem(uint64_t* pool, uint8_t* aux, int64_t P, int64_t k,
+                                              int lognb, int nt) {
+  RankSmem S;
+  S.pool = pool;
+  S.hist = reinterpret_cast<uint32_t*>(aux);
+  aux += ((size_t)((1 << lognb) + 2) * 4 + 127) / 128 * 128;
+  S.inv = reinterpret_cast<uint16_t*>(aux);
+  aux += ((size_t)k * 2 + 127) / 128 * 128;
+  S.bid = reinterpret_cast<uint16_t*>(aux);
+  aux += ((size_t)P * 2 + 127) / 128 * 128;
+  S.work = reinterpret_cast<int2*>(aux);
+  aux += (size_t)RS_WORK * 8;
+  S.red = reinterpret_cast<uint64_t*>(aux);
+  aux += (size_t)(nt / 32) * 24;
+  S.ctl = reinterpret_cast<int*>(aux);
+  return S;
+}
+
+// Choose log2(#buckets) for a pool of P keys: ~2 keys per bucket, 256..4096
+// (bucket ids are 16-bit; the in-bucket count costs ~bucket size per key).
 __host__ __device__ inline int rank_lognb(int64_t P) {
   int l = 8;
-  while (l < 12 && ((int64_t)1 << (l + 2)) < P) ++l;
+  while (l < 12 && ((int64_t)1 << (l + 1)) < P) ++l;
   return l;
 }
 

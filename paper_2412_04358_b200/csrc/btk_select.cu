@@ -41,17 +41,7 @@ __global__ void __launch_bounds__(NT) k2_small(const uint64_t* __restrict__ in, 
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw);
   uint8_t* aux = smem_raw + ((size_t)L * 8 + 127) / 128 * 128;
-  RankSmem S;
-  S.pool = sk;
-  S.hist = reinterpret_cast<uint32_t*>(aux);
-  aux += ((size_t)((1 << lognb) + 2) * 4 + 127) / 128 * 128;
-  S.inv = reinterpret_cast<uint16_t*>(aux);
-  aux += ((size_t)kk * 2 + 127) / 128 * 128;
-  S.work = reinterpret_cast<int2*>(aux);
-  aux += (size_t)RS_WORK * 8;
-  S.red = reinterpret_cast<uint64_t*>(aux);
-  aux += (size_t)(NT / 32) * 24;
-  S.ctl = reinterpret_cast<int*>(aux);
+  const RankSmem S = rank_smem(sk, aux, L, kk, lognb, NT);
   const int64_t seg = blockIdx.x;
   const uint64_t* src = in + seg * in_stride;
   for (int p = threadIdx.x; p < L; p += NT) sk[p] = src[p];
@@ -219,7 +209,7 @@ template <int DT, int NT, int ITEMS, bool DECODE>
 static cudaError_t launch_small(const K2Args& a, cudaStream_t st) {
   auto kern = k2_small<DT, NT, ITEMS, DECODE>;
   const int lognb = rank_lognb(a.L);
-  const size_t sm = ((size_t)a.L * 8 + 127) / 128 * 128 + rank_aux_bytes(NT, lognb, a.kk);
+  const size_t sm = ((size_t)a.L * 8 + 127) / 128 * 128 + rank_aux_bytes(NT, lognb, a.kk, a.L);
   cudaError_t e = ensure_smem_attr((const void*)kern, sm);
   if (e != cudaSuccess) return e;
   if (a.nseg == 0) return cudaSuccess;

@@ -19,6 +19,7 @@ nb = 8192
 buf = np.zeros((nb, 8), np.uint64)
 rc = op.lib.btk_trace_read(ctypes.c_void_p(buf.ctypes.data), nb)
 t = buf.astype(np.float64)
+t[:, 1] = np.where(t[:, 1] > 0, t[:, 1], t[:, 0])
 used = t[:, 0] > 0
 t = t[used]
 t0 = t[:, 0].min()
