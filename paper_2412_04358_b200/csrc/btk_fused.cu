@@ -639,110 +639,6 @@ struct RowsArgs {
   uint32_t* flag;
 };
 
-template <int DT, int ITEMS>
-__device__ __forceinline__ void warp_rank_sort(uint64_t* pool, int P, int k, uint16_t* inv,
-                                               uint16_t* bid, uint32_t* hist, int lognb, int ib) {
-  const int lane = threadIdx.x & 31;
-  for (int q = lane; q < k; q += 32) inv[q] = RS_NONE;
-  uint64_t key[ITEMS];
-  uint32_t slot[ITEMS];
-  uint64_t mn = ~0ull, mx = 0ull;
-  float vmn = __int_as_float(0x7F800000), vmx = -__int_as_float(0x7F800000);
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const int p = lane + 32 * i;
-    key[i] = p < P ? pool[p] : 0ull;
-    if (key[i]) {
-      mn = key[i] < mn ? key[i] : mn;
-      mx = key[i] > mx ? key[i] : mx;
-      const float v = comp_value<DT>(key[i], ib);
-      vmn = fminf(vmn, v);
-      vmx = fmaxf(vmx, v);
-    }
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    const uint64_t a = __shfl_xor_sync(0xFFFFFFFFu, mn, o);
-    const uint64_t b = __shfl_xor_sync(0xFFFFFFFFu, mx, o);
-    mn = a < mn ? a : mn;
-    mx = b > mx ? b : mx;
-    vmn = fminf(vmn, __shfl_xor_sync(0xFFFFFFFFu, vmn, o));
-    vmx = fmaxf(vmx, __shfl_xor_sync(0xFFFFFFFFu, vmx, o));
-  }
-  if (mx == 0ull) { __syncwarp(); return; }
-  RsRule R;
-  R.nb = 1 << lognb;
-  R.mn = mn;
-  R.vmx = vmx;
-  R.same = (mn == mx);
-  R.shift = max(0, bits64(mx - mn) - lognb);
-  const float span = vmx - vmn;
-  R.scale = (float)R.nb / span;
-  const bool narrow_band = (vmn > 0.f && vmx < 4.f * vmn) || (vmx < 0.f && vmn > 4.f * vmx);
-  R.vmode = !narrow_band && (span > 0.f) && (R.scale > 0.f) && (R.scale < 3.0e38f) &&
-            (span < 3.0e38f);
-  for (int j = lane; j < R.nb + 2; j += 32) hist[j] = 0u;
-  __syncwarp();
-  uint16_t dd[ITEMS];
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    if (lane + 32 * i < P) {
-      dd[i] = (uint16_t)rs_bucket<DT>(R, key[i], ib);
-      slot[i] = atomicAdd(&hist[dd[i]], 1u);
-    }
-  }
-  __syncwarp();
-  {  // warp exclusive scan of hist[0 .. nb+2)
-    const int len = R.nb + 2, chunk = (len + 31) / 32, b0 = lane * chunk;
-    uint32_t sum = 0;
-    for (int i = 0; i < chunk; ++i) sum += (b0 + i < len) ? hist[b0 + i] : 0u;
-    uint32_t incl = sum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    uint32_t run = incl - sum;
-    __syncwarp();
-    for (int i = 0; i < chunk; ++i) {
-      if (b0 + i < len) {
-        const uint32_t c = hist[b0 + i];
-        hist[b0 + i] = run;
-        run += c;
-      }
-    }
-  }
-  __syncwarp();
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    if (lane + 32 * i < P) {
-      const int q = (int)hist[dd[i]] + (int)slot[i];
-      pool[q] = key[i];
-      bid[q] = dd[i];
-    }
-  }
-  __syncwarp();
-  for (int p = lane; p < P; p += 32) {
-    const uint64_t x = pool[p];
-    if (!x) continue;
-    if (R.same) {
-      if (p < k) inv[p] = (uint16_t)p;
-      continue;
-    }
-    const int d = bid[p];
-    const int s0 = (int)hist[d], s1 = (int)hist[d + 1];
-    if (s0 >= k) continue;
-    int cnt = 0;
-    for (int j = s0; j < s1; ++j) {
-      const uint64_t y = pool[j];
-      cnt += (y > x || (y == x && j < p)) ? 1 : 0;
-    }
-    const int f = s0 + cnt;
-    if (f < k) inv[f] = (uint16_t)p;
-  }
-  __syncwarp();
-}
-
 template <int DT, int KB, int GPL, int U, int ITEMS>
 __global__ void __launch_bounds__(256) fused_rows(RowsArgs a) {
   constexpr int V = Vec<DT>::V;

@@ -260,3 +260,28 @@ def test_fused_launch_shapes_match_oracle(env, monkeypatch):
                 x = torch.from_numpy(x32).to(DT[dn]).cuda()
                 r = btk.approx_topk(x, k, btk.BucketScheme(b, kb, I))
                 assert_same(r, wv, wi, DT[dn])
+
+
+@pytest.mark.parametrize("kind", ["two_values", "one_outlier", "all_equal", "normal_bf16"])
+def test_long_segment_cluster_and_fallback(kind):
+    """Segments of 16K-128K keys go to the cluster kernel; adversarially
+    skewed value distributions overflow its per-CTA buffers and must take
+    the radix-select fallback for exactly those segments (mixed here)."""
+    rng = np.random.default_rng(5)
+    m, n, k = 3, 120000, 60000
+    x32 = rng.standard_normal((m, n), dtype=np.float32)
+    if kind == "two_values":
+        x32[0] = rng.integers(0, 2, size=n).astype(np.float32)
+    elif kind == "one_outlier":
+        x32[1] = 1.0
+        x32[1, 777] = 1e30
+    elif kind == "all_equal":
+        x32[2] = -2.5
+    dt = torch.bfloat16 if kind == "normal_bf16" else torch.float32
+    if dt == torch.bfloat16:
+        x32 = torch.from_numpy(x32).to(dt).float().numpy()
+    wv, wi = O.approx_topk(x32, k, 1, k)  # exact (b = 1): one long segment per row
+    r = btk.approx_topk(torch.from_numpy(x32).to(dt).cuda(), k, btk.BucketScheme(1, k, I))
+    assert_same(r, wv, wi, dt)
+    e = btk.exact_topk_oracle(torch.from_numpy(x32).to(dt).cuda(), k)
+    assert_same(e, wv, wi, dt)
