@@ -35,10 +35,8 @@ CompGeo geo_for(int dtype, int64_t space) {
 
 // Workspace carve-up of the generic path.
 struct Plan {
-  size_t pool = 0, mat = 0, s1a = 0, s1b = 0, s2a = 0, s2b = 0, s2f = 0;
-  size_t total() const {
-    return al(pool) + al(mat) + al(s1a) + al(s1b) + al(s2a) + al(s2b) + al(s2f);
-  }
+  size_t pool = 0, mat = 0, s1a = 0, s1b = 0, s2a = 0, s2b = 0;
+  size_t total() const { return al(pool) + al(mat) + al(s1a) + al(s1b) + al(s2a) + al(s2b); }
 };
 
 Plan plan_generic(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb) {
@@ -46,10 +44,7 @@ Plan plan_generic(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb) {
   const int64_t s = ceil_div(n, b);
   if (b == 1) {
     pl.mat = (size_t)(m * n * 8);
-    if (n > K2_SMALL_CAP) {
-      pl.s2a = pl.s2b = (size_t)(m * kb * 8);
-      pl.s2f = (size_t)(m * 4);
-    }
+    if (n > K2_SMALL_CAP) pl.s2a = pl.s2b = (size_t)(m * kb * 8);
     return pl;
   }
   pl.pool = (size_t)(m * b * kb * 8);
@@ -57,10 +52,7 @@ Plan plan_generic(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb) {
     pl.mat = (size_t)(m * b * s * 8);
     if (s > K2_SMALL_CAP) pl.s1a = pl.s1b = (size_t)(m * b * kb * 8);
   }
-  if (b * kb > K2_SMALL_CAP) {
-    pl.s2a = pl.s2b = (size_t)(m * k * 8);
-    pl.s2f = (size_t)(m * 4);
-  }
+  if (b * kb > K2_SMALL_CAP) pl.s2a = pl.s2b = (size_t)(m * k * 8);
   return pl;
 }
 
@@ -206,13 +198,12 @@ int btk_approx_topk(const void* x, int64_t row_stride, int dtype, int64_t m, int
     cv.take(pl.pool);
     uint64_t* s2a = cv.take(pl.s2a);
     uint64_t* s2b = cv.take(pl.s2b);
-    uint32_t* s2f = reinterpret_cast<uint32_t*>(cv.take(pl.s2f));
     rc = cuda_status(run_materialize(p, mat, st));
     if (rc) return rc;
     K2Args a{};
     a.in = mat; a.in_stride = n; a.nseg = m; a.L = n; a.kk = k;
     a.out_vals = out_vals; a.out_idx = out_idx; a.out_stride = k;
-    a.geo = p.geo; a.scratch_a = s2a; a.scratch_b = s2b; a.seg_flag = s2f;
+    a.geo = p.geo; a.scratch_a = s2a; a.scratch_b = s2b;
     return cuda_status(run_k2(dtype, true, a, st));
   }
   uint64_t* pool = cv.take(pl.pool);
@@ -222,11 +213,10 @@ int btk_approx_topk(const void* x, int64_t row_stride, int dtype, int64_t m, int
   cv.take(pl.mat); cv.take(pl.s1a); cv.take(pl.s1b);
   uint64_t* s2a = cv.take(pl.s2a);
   uint64_t* s2b = cv.take(pl.s2b);
-  uint32_t* s2f = reinterpret_cast<uint32_t*>(cv.take(pl.s2f));
   K2Args a{};
   a.in = pool; a.in_stride = b * kb; a.nseg = m; a.L = b * kb; a.kk = k;
   a.out_vals = out_vals; a.out_idx = out_idx; a.out_stride = k;
-  a.geo = p.geo; a.scratch_a = s2a; a.scratch_b = s2b; a.seg_flag = s2f;
+  a.geo = p.geo; a.scratch_a = s2a; a.scratch_b = s2b;
   return cuda_status(run_k2(dtype, true, a, st));
 }
 
@@ -313,7 +303,7 @@ size_t btk_topk_with_indices_workspace_bytes(int64_t m, int64_t c, int64_t k, in
   (void)dtype;
   if (m < 1 || c < 1 || k < 1 || k > c) return 0;
   size_t v = al((size_t)(m * c * 8));
-  if (c > K2_SMALL_CAP) v += 2 * al((size_t)(m * k * 8)) + al((size_t)(m * 4));
+  if (c > K2_SMALL_CAP) v += 2 * al((size_t)(m * k * 8));
   return v;
 }
 
@@ -332,7 +322,6 @@ int btk_topk_with_indices(const void* values, const int64_t* labels, int dtype, 
   uint64_t* comps = cv.take((size_t)(m * c * 8));
   uint64_t* sa = c > K2_SMALL_CAP ? cv.take((size_t)(m * k * 8)) : nullptr;
   uint64_t* sb = c > K2_SMALL_CAP ? cv.take((size_t)(m * k * 8)) : nullptr;
-  uint32_t* sf = c > K2_SMALL_CAP ? reinterpret_cast<uint32_t*>(cv.take((size_t)(m * 4))) : nullptr;
   const int64_t total = m * c;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 64));
   switch (dtype) {
@@ -345,7 +334,7 @@ int btk_topk_with_indices(const void* values, const int64_t* labels, int dtype, 
   K2Args a{};
   a.in = comps; a.in_stride = c; a.nseg = m; a.L = c; a.kk = k;
   a.out_vals = out_vals; a.out_idx = out_idx; a.out_stride = k;
-  a.geo = g; a.scratch_a = sa; a.scratch_b = sb; a.seg_flag = sf;
+  a.geo = g; a.scratch_a = sa; a.scratch_b = sb;
   return cuda_status(run_k2(dtype, true, a, st));
 }
 

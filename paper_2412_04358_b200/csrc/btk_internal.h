@@ -26,7 +26,6 @@ struct K2Args {
   CompGeo geo;
   uint64_t* scratch_a;  // long segments only: nseg * kk keys each
   uint64_t* scratch_b;
-  uint32_t* seg_flag;   // long segments: nseg flags (cluster path -> fallback); may be null
 };
 
 // Opt a kernel into >48 KB dynamic smem once per device (never during
