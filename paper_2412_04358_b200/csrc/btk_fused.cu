@@ -569,6 +569,10 @@ __global__ void __launch_bounds__(NT) fused_narrow(NarrowArgs a) {
   uint64_t* pool = reinterpret_cast<uint64_t*>(smem + a.pool_off);
   if (active) sc.template spill<KB>(scratch + (int64_t)r * b * KB, g, b, t_begin, a.geo);
   __syncthreads();
+  // fold the R phase queues and push the CTA's partial straight into the
+  // leader's slot c (DSMEM store for c > 0): one cluster barrier, no remote
+  // reads
+  uint64_t* dst = (a.S > 1) ? cluster.map_shared_rank(part, 0) + (int64_t)crank * b * KB : part;
   for (int64_t j = tid; j < b; j += NT) {
     uint64_t best[KB];
 #pragma unroll
@@ -578,29 +582,25 @@ __global__ void __launch_bounds__(NT) fused_narrow(NarrowArgs a) {
       for (int z = 0; z < KB; ++z) comp_push<KB>(best, scratch[((int64_t)rr * b + j) * KB + z]);
     }
 #pragma unroll
-    for (int z = 0; z < KB; ++z) part[j * KB + z] = best[z];
+    for (int z = 0; z < KB; ++z) dst[j * KB + z] = best[z];
   }
   const bool anybad = __syncthreads_or(bad);
   if (anybad && tid == 0 && a.flag) atomicOr(a.flag, 1u);
-
-  // ---- cluster merge through DSMEM into the leader's pool
-  if (a.S > 1) cluster.sync();
+  if (a.S > 1) cluster.sync();  // all partials delivered to the leader
   if (crank == 0) {
     for (int64_t j = tid; j < b; j += NT) {
       uint64_t best[KB];
 #pragma unroll
       for (int z = 0; z < KB; ++z) best[z] = part[j * KB + z];
       for (int c = 1; c < a.S; ++c) {
-        const uint64_t* rp = cluster.map_shared_rank(part, c);
 #pragma unroll
-        for (int z = 0; z < KB; ++z) comp_push<KB>(best, rp[j * KB + z]);
+        for (int z = 0; z < KB; ++z) comp_push<KB>(best, part[((int64_t)c * b + j) * KB + z]);
       }
 #pragma unroll
       for (int z = 0; z < KB; ++z)
         if (z < a.kb) pool[j * a.kb + z] = best[z];
     }
   }
-  if (a.S > 1) cluster.sync();  // remote partials stay alive until read
   if (tr) g_trace[blockIdx.x][3] = gtime();
   if (crank != 0) {
     if (tr) g_trace[blockIdx.x][4] = gtime();
@@ -855,14 +855,6 @@ bool plan_narrow(const Problem& p, Plan& pl) {
   a.sort_items = sort_items_for(P, NT);
   if (a.sort_items > 32) return false;  // engine keys per thread
   a.lognb = rank_lognb(P);
-  const int kbt = kb_tmpl(p.kb);
-  const size_t scratch = (size_t)a.R * p.b * kbt * 8;
-  const size_t regA = a16(scratch);
-  a.scratch_off = 0;
-  a.part_off = regA;
-  a.pool_off = regA + a16((size_t)p.b * kbt * 8);
-  a.aux_off = a.pool_off + (P <= 64 ? 64 * 8 : a16((size_t)P * 8));
-  const size_t post = a.pool_off + stage2_bytes(P, p.k, NT);
   // Launch shape (measured on B200, tools/sweep_narrow2.sh): rows of >= 1 MB
   // run one CTA per row with a deep ring (3 x 48 KB in flight; cfg3 94% of
   // the copy peak); shorter rows split over a cluster of S CTAs so about
@@ -876,6 +868,17 @@ bool plan_narrow(const Problem& p, Plan& pl) {
   if (env_int("BTK_S", 0)) S = env_int("BTK_S", 0);
   while (S < 8 && (s + S - 1) / S >= 0xFFFF) S *= 2;  // 16-bit slot codes of the packed scanner
   if (S > s || (s + S - 1) / S >= 0xFFFF) return false;
+  const int kbt = kb_tmpl(p.kb);
+  const size_t scratch = (size_t)a.R * p.b * kbt * 8;
+  const size_t regA = a16(scratch);
+  // post-scan layout aliases the ring (scratch, pool, engine scratch); the
+  // S partial slots the cluster CTAs push into live beyond both, because a
+  // finished CTA may push while the leader is still streaming
+  a.scratch_off = 0;
+  a.pool_off = regA;
+  a.aux_off = a.pool_off + (P <= 64 ? 64 * 8 : a16((size_t)P * 8));
+  const size_t post = a.pool_off + stage2_bytes(P, p.k, NT);
+  const size_t part_bytes = (size_t)S * p.b * kbt * 8;
   const bool deep = row_bytes / S >= (1 << 20);
   int NS = env_int("BTK_NS", deep ? 3 : 2);
   int stage_kb = env_int("BTK_STAGE_KB", deep ? 48 : 32);
@@ -886,10 +889,12 @@ bool plan_narrow(const Problem& p, Plan& pl) {
     if (T * vrow_bytes > 64 * 1024) return false;
     const int64_t stages = ((s + S - 1) / S + T - 1) / T;
     const int ns = (int)std::min<int64_t>(std::min<int64_t>(stages, NS), MAX_STAGES);
-    const size_t sm = std::max(post, (size_t)ns * (size_t)(T * vrow_bytes));
+    const size_t part_off = a16(std::max(post, (size_t)ns * (size_t)(T * vrow_bytes)));
+    const size_t sm = part_off + part_bytes;
     if (sm <= SMEM_LIMIT || stage_kb <= 8) {
       a.T = (int)T;
       a.stage_bytes = (size_t)(T * vrow_bytes);
+      a.part_off = part_off;
       NS = ns;
       smem = sm;
       break;

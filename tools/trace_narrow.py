@@ -28,10 +28,14 @@ names = ["start", "first_stage", "stream_done", "merged", "end", "ranked"]
 print(cfg, "CTAs traced", used.sum(), "rc", rc)
 sm = buf[used][:, 6].astype(np.int64) % 4096
 print("distinct SMs", len(np.unique(sm)), "CTAs/SM max", np.bincount(sm.astype(np.int64)).max())
+ok5 = r[:, 5] > 0
 d = r[:, 5] - r[:, 3]
-print("rank phase (ranked - merged): p50 %.2f us  p90 %.2f" % (np.median(d[r[:, 5] > 0]), np.percentile(d[r[:, 5] > 0], 90)))
-d = r[:, 4] - r[:, 5]
-print("emit phase (end - ranked): p50 %.2f us" % np.median(d[r[:, 5] > 0]))
+if ok5.any():
+    print("rank phase (ranked - merged): p50 %.2f us  p90 %.2f" % (np.median(d[ok5]), np.percentile(d[ok5], 90)))
+    d = r[:, 4] - r[:, 5]
+    print("emit phase (end - ranked): p50 %.2f us" % np.median(d[ok5]))
 for j, nm in enumerate(names):
     col = r[:, j]
+    if j == 5 and not ok5.any():
+        continue
     print(f"{nm:>12}: min {col.min():7.2f}  p10 {np.percentile(col,10):7.2f}  p50 {np.median(col):7.2f}  p90 {np.percentile(col,90):7.2f}  max {col.max():7.2f} us")
