@@ -12,7 +12,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbtk.so")
+# BTK_LIB overrides the library file (development A/B runs of two builds)
+LIB_PATH = os.environ.get("BTK_LIB") or os.path.join(_HERE, "libbtk.so")
 
 BTK_F32, BTK_BF16, BTK_F16 = 0, 1, 2
 BTK_INTERLEAVED, BTK_CONTIGUOUS = 0, 1

@@ -482,6 +482,7 @@ struct NarrowArgs {
 template <int DT, int KB, int NT, int ITEMS>
 __global__ void __launch_bounds__(NT) fused_narrow(NarrowArgs a) {
   constexpr int V = Vec<DT>::V;
+  constexpr int LB = (KB <= 2) ? 8 : 4;  // smem vectors in flight per thread
   constexpr int ESZ = VT<DT>::W / 8;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[MAX_STAGES];
@@ -548,8 +549,19 @@ __global__ void __launch_bounds__(NT) fused_narrow(NarrowArgs a) {
     if (active) {
       uint32_t addr = smem_base + (uint32_t)(slot * a.stage_bytes) + (uint32_t)(r * b * ESZ);
       const int trel0 = (int)(t0 - t_begin);
-#pragma unroll 4
-      for (int rr = r; rr < rows_main; rr += R) {
+      // LB shared-memory loads issued back to back, then consumed: the scan
+      // of a stage is issue/latency-bound once HBM delivers (cfg3: one CTA
+      // per SM), so the loads must not wait on the previous row's compute
+      int rr = r;
+      for (; rr + (LB - 1) * R < rows_main; rr += LB * R) {
+        uint4 v[LB];
+#pragma unroll
+        for (int u = 0; u < LB; ++u) v[u] = lds128(addr + (uint32_t)u * row_step);
+#pragma unroll
+        for (int u = 0; u < LB; ++u) sc.row(v[u], trel0 + rr + u * R);
+        addr += (uint32_t)LB * row_step;
+      }
+      for (; rr < rows_main; rr += R) {
         sc.row(lds128(addr), trel0 + rr);
         addr += row_step;
       }
