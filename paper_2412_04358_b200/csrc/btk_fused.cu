@@ -66,6 +66,9 @@ constexpr int WIDE_U = 8;                  // 16-byte loads in flight per thread
 constexpr int64_t FUSED_POOL_CAP = 16384;  // survivors sorted in smem
 constexpr size_t SMEM_LIMIT = 225 * 1024;  // dynamic; leaves room for static smem
 constexpr int MAX_STAGES = 8;
+#ifndef ROWS_MINB
+#define ROWS_MINB 2
+#endif
 constexpr int NUM_SMS = 148;
 
 template <int DT> struct Vec;
@@ -652,7 +655,7 @@ struct RowsArgs {
 };
 
 template <int DT, int KB, int GPL, int U, int ITEMS>
-__global__ void __launch_bounds__(256) fused_rows(RowsArgs a) {
+__global__ void __launch_bounds__(256, ROWS_MINB) fused_rows(RowsArgs a) {
   constexpr int V = Vec<DT>::V;
   constexpr int ESZ = VT<DT>::W / 8;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -672,21 +675,34 @@ __global__ void __launch_bounds__(256) fused_rows(RowsArgs a) {
     Scanner<DT, KB> sc[GPL];
 #pragma unroll
     for (int j = 0; j < GPL; ++j) sc[j].init();
+    // all GPL columns' loads of U view-rows in flight together (GPL*U
+    // 16-byte loads per lane); the ragged final view-row, if any, last
+    const int64_t s_full = (a.last_vec < G) ? s - 1 : s;
+    int64_t t0 = 0;
+    for (; t0 + U <= s_full; t0 += U) {
+      uint4 v[GPL][U];
+#pragma unroll
+      for (int j = 0; j < GPL; ++j) {
+        const int g = lane + 32 * j;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          v[j][u] = (g < G) ? ldg_stream(rowp + ((t0 + u) * b + (int64_t)g * V) * ESZ) : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int j = 0; j < GPL; ++j) {
+        if (lane + 32 * j < G) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) sc[j].row(v[j][u], (int)(t0 + u));
+        }
+      }
+    }
 #pragma unroll
     for (int j = 0; j < GPL; ++j) {
       const int g = lane + 32 * j;
       if (g < G) {
-        const uint8_t* colp = rowp + (int64_t)g * V * ESZ;
         const int64_t s_eff = (g < a.last_vec) ? s : s - 1;
-        int64_t t0 = 0;
-        for (; t0 + U <= s_eff; t0 += U) {
-          uint4 v[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) v[u] = ldg_stream(colp + (t0 + u) * b * ESZ);
-#pragma unroll
-          for (int u = 0; u < U; ++u) sc[j].row(v[u], (int)(t0 + u));
-        }
-        for (; t0 < s_eff; ++t0) sc[j].row(ldg_stream(colp + t0 * b * ESZ), (int)t0);
+        for (int64_t t = t0; t < s_eff; ++t)
+          sc[j].row(ldg_stream(rowp + (t * b + (int64_t)g * V) * ESZ), (int)t);
       }
     }
 #pragma unroll
@@ -1041,7 +1057,7 @@ cudaError_t launch_wide(const Plan& pl, cudaStream_t st) {
 
 template <int DT, int KB, int GPL, int ITEMS>
 cudaError_t launch_rows_t(const Plan& pl, cudaStream_t st) {
-  constexpr int U = GPL == 1 ? 8 : 4;
+  constexpr int U = (GPL == 1 ? 8 : 4) / (KB > 2 ? 2 : 1);
   auto kern = fused_rows<DT, KB, GPL, U, ITEMS>;
   cudaError_t e = ensure_smem_attr((const void*)kern, pl.smem);
   if (e != cudaSuccess) return e;
