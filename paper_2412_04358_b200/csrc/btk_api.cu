@@ -335,6 +335,7 @@ int btk_topk_with_indices(const void* values, const int64_t* labels, int dtype, 
   a.in = comps; a.in_stride = c; a.nseg = m; a.L = c; a.kk = k;
   a.out_vals = out_vals; a.out_idx = out_idx; a.out_stride = k;
   a.geo = g; a.scratch_a = sa; a.scratch_b = sb;
+  a.unique = false;  // carried labels may repeat
   return cuda_status(run_k2(dtype, true, a, st));
 }
 

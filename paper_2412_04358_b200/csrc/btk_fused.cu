@@ -870,7 +870,7 @@ bool common_envelope(const Problem& p) {
 bool plan_narrow(const Problem& p, Plan& pl) {
   const int V = vec_of(p.dtype), esz = esz_of(p.dtype);
   const int64_t G = p.b / V, s = (p.n + p.b - 1) / p.b, P = p.b * p.kb;
-  const int NT = G <= 16 ? 128 : 256;
+  const int NT = env_int("BTK_NT", 0) == 256 ? 256 : (G <= 16 ? 128 : 256);
   if (G > NT) return false;
   NarrowArgs& a = pl.na;
   a.x = p.x; a.row_stride = p.row_stride;

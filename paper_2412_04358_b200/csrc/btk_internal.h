@@ -26,6 +26,7 @@ struct K2Args {
   CompGeo geo;
   uint64_t* scratch_a;  // long segments only: nseg * kk keys each
   uint64_t* scratch_b;
+  bool unique = true;   // keys unique (false: repeated carried labels possible)
 };
 
 // Opt a kernel into >48 KB dynamic smem once per device (never during

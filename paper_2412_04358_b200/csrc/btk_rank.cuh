@@ -43,6 +43,25 @@ __device__ __forceinline__ uint64_t rs_key(const uint64_t* pool, uint16_t pos) {
   return pos == RS_NONE ? 0ull : pool[pos];
 }
 
+// #keys of bucket [s0, s1) ranked before key x at position p.  UNIQ: keys
+// are unique (every composite key carries its index; only carried labels
+// of topk_with_indices can repeat), so only "greater" counts.
+template <bool UNIQ>
+__device__ __forceinline__ int rs_count_greater(const uint64_t* pool, int s0, int s1, uint64_t x,
+                                                int p) {
+  int cnt = 0;
+  if constexpr (UNIQ) {
+#pragma unroll 4
+    for (int j = s0; j < s1; ++j) cnt += pool[j] > x ? 1 : 0;
+  } else {
+    for (int j = s0; j < s1; ++j) {
+      const uint64_t y = pool[j];
+      cnt += (y > x || (y == x && j < p)) ? 1 : 0;
+    }
+  }
+  return cnt;
+}
+
 struct RankSmem {
   uint64_t* pool;   // P keys (permuted in place)
   uint16_t* inv;    // >= k entries
@@ -152,7 +171,7 @@ __device__ __forceinline__ int rs_bucket(const RsRule& r, uint64_t key, int ib) 
 
 // Bucket one range [lo, hi) of the pool, rank its small buckets, queue the
 // big ones.  All NT threads call it with identical arguments.
-template <int DT, int NT, int ITEMS>
+template <int DT, int NT, int ITEMS, bool UNIQ = true>
 __device__ __forceinline__ void rs_range(const RankSmem& S, int lo, int hi, int k, int lognb,
                                          int ib) {
   const int tid = threadIdx.x;
@@ -228,11 +247,7 @@ __device__ __forceinline__ void rs_range(const RankSmem& S, int lo, int hi, int 
       }
       continue;
     }
-    int cnt = 0;
-    for (int j = s0; j < s1; ++j) {
-      const uint64_t y = S.pool[lo + j];
-      cnt += (y > x || (y == x && j < p)) ? 1 : 0;
-    }
+    const int cnt = rs_count_greater<UNIQ>(S.pool + lo, s0, s1, x, p);
     const int f = lo + s0 + cnt;
     if (f < k) S.inv[f] = (uint16_t)(lo + p);
   }
@@ -242,19 +257,19 @@ __device__ __forceinline__ void rs_range(const RankSmem& S, int lo, int hi, int 
 // Full engine: after return (and a barrier), inv[0 .. min(k, #non-empty))
 // holds pool positions in canonical order.  P <= NT * ITEMS, P <= 16384.
 // ib = index bits of the composite keys (CompGeo::ib).
-template <int DT, int NT, int ITEMS>
+template <int DT, int NT, int ITEMS, bool UNIQ = true>
 __device__ void rank_select_sort(const RankSmem& S, int P, int k, int lognb, int ib) {
   if (threadIdx.x == 0) { S.ctl[0] = 0; S.ctl[1] = 0; }
   for (int q = threadIdx.x; q < k; q += NT) S.inv[q] = RS_NONE;
   __syncthreads();
-  rs_range<DT, NT, ITEMS>(S, 0, P, k, lognb, ib);
+  rs_range<DT, NT, ITEMS, UNIQ>(S, 0, P, k, lognb, ib);
   for (;;) {
     const int head = S.ctl[0], tail = S.ctl[1];
     if (head >= tail) break;
     const int2 r = S.work[head % RS_WORK];
     __syncthreads();
     if (threadIdx.x == 0) S.ctl[0] = head + 1;
-    rs_range<DT, NT, ITEMS>(S, r.x, r.y, k, lognb, ib);
+    rs_range<DT, NT, ITEMS, UNIQ>(S, r.x, r.y, k, lognb, ib);
   }
   __syncthreads();
 }
@@ -262,7 +277,7 @@ __device__ void rank_select_sort(const RankSmem& S, int P, int k, int lognb, int
 // Warp-synchronous form of the engine for one warp's pool of P <= 32*ITEMS
 // keys (fused_rows; big buckets of k2_cluster): one bucketing level, then
 // in-bucket counting with no size limit.  inv[f] = pos_off + position.
-template <int DT, int ITEMS>
+template <int DT, int ITEMS, bool UNIQ = true>
 __device__ __forceinline__ void warp_rank_sort(uint64_t* pool, int P, int k, uint16_t* inv,
                                                uint16_t* bid, uint32_t* hist, int lognb, int ib,
                                                int pos_off = 0) {
@@ -356,11 +371,7 @@ __device__ __forceinline__ void warp_rank_sort(uint64_t* pool, int P, int k, uin
     const int d = bid[p];
     const int s0 = (int)hist[d], s1 = (int)hist[d + 1];
     if (s0 >= k) continue;
-    int cnt = 0;
-    for (int j = s0; j < s1; ++j) {
-      const uint64_t y = pool[j];
-      cnt += (y > x || (y == x && j < p)) ? 1 : 0;
-    }
+    const int cnt = rs_count_greater<UNIQ>(pool, s0, s1, x, p);
     const int f = s0 + cnt;
     if (f < k) inv[f] = (uint16_t)(pos_off + p);
   }

@@ -32,7 +32,7 @@ __device__ __forceinline__ void emit(uint64_t c, int64_t pos, const CompGeo& g, 
 // ---------------------------------------------------------------------------
 // One CTA per segment of L <= NT*ITEMS keys: keys into shared memory, the
 // bucketing/rank engine (btk_rank.cuh) finds the kk largest in order.
-template <int DT, int NT, int ITEMS, bool DECODE>
+template <int DT, int NT, int ITEMS, bool DECODE, bool UNIQ>
 __global__ void __launch_bounds__(NT) k2_small(const uint64_t* __restrict__ in, int64_t in_stride,
                                                int64_t L, int64_t kk, uint64_t* __restrict__ out_keys,
                                                void* __restrict__ out_vals,
@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(NT) k2_small(const uint64_t* __restrict__ in, 
   const uint64_t* src = in + seg * in_stride;
   for (int p = threadIdx.x; p < L; p += NT) sk[p] = src[p];
   __syncthreads();
-  rank_select_sort<DT, NT, ITEMS>(S, (int)L, (int)kk, lognb, g.ib);
+  rank_select_sort<DT, NT, ITEMS, UNIQ>(S, (int)L, (int)kk, lognb, g.ib);
   // fewer than kk non-empty keys (only via empty slots): pad with 0 = "empty"
   for (int p = threadIdx.x; p < kk; p += NT) {
     const uint64_t c = rs_key(sk, S.inv[p]);
@@ -207,7 +207,7 @@ __global__ void k2_decode(const uint64_t* __restrict__ in, int64_t in_stride, in
 // Host dispatch.
 template <int DT, int NT, int ITEMS, bool DECODE>
 static cudaError_t launch_small(const K2Args& a, cudaStream_t st) {
-  auto kern = k2_small<DT, NT, ITEMS, DECODE>;
+  auto kern = a.unique ? k2_small<DT, NT, ITEMS, DECODE, true> : k2_small<DT, NT, ITEMS, DECODE, false>;
   const int lognb = rank_lognb(a.L);
   const size_t sm = ((size_t)a.L * 8 + 127) / 128 * 128 + rank_aux_bytes(NT, lognb, a.kk, a.L);
   cudaError_t e = ensure_smem_attr((const void*)kern, sm);
