@@ -239,39 +239,8 @@ __device__ __forceinline__ void emit_comp(uint64_t c, int64_t pos, const CompGeo
   out_idx[pos] = idx;
 }
 
-// 64-key bitonic sort (descending) by one warp; keys in sk[0..63].
-__device__ __forceinline__ void warp_sort64_desc(uint64_t* sk) {
-  const int lane = threadIdx.x & 31;
-  uint64_t x[2] = {sk[lane], sk[lane + 32]};
-#pragma unroll
-  for (int size = 2; size <= 64; size <<= 1) {
-#pragma unroll
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      if (stride == 32) {
-        const uint64_t hi = x[0] > x[1] ? x[0] : x[1];
-        const uint64_t lo = x[0] > x[1] ? x[1] : x[0];
-        x[0] = hi;
-        x[1] = lo;
-      } else {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int i = lane + 32 * h;
-          const uint64_t y = __shfl_xor_sync(0xFFFFFFFFu, x[h], stride);
-          const bool lower = (i & stride) == 0;
-          const bool desc = (i & size) == 0;
-          const uint64_t mx = x[h] > y ? x[h] : y;
-          const uint64_t mn = x[h] > y ? y : x[h];
-          x[h] = (lower == desc) ? mx : mn;
-        }
-      }
-    }
-  }
-  sk[lane] = x[0];
-  sk[lane + 32] = x[1];
-}
-
-// Stage 2 of one row's pool: the P survivors (ITEMS == 0, P <= 64: warp
-// bitonic sort of a zero-padded 64-key tile; else the bucketing/rank engine
+// Stage 2 of one row's pool: the P survivors (ITEMS == 0, P <= 64: rank by
+// counting; else the bucketing/rank engine
 // of btk_rank.cuh with ITEMS >= P/NT keys per thread), then the canonical
 // write of the first k.  `aux` is the engine's shared-memory scratch
 // (rank_aux_bytes).  ITEMS is exact per kernel instance so the register
@@ -282,12 +251,17 @@ __device__ __forceinline__ void stage2_emit(uint64_t* pool, uint8_t* aux, int64_
                                             int lognb, int64_t row, const CompGeo& geo,
                                             void* out_vals, int64_t* out_idx, bool trace_on = false) {
   if constexpr (ITEMS == 0) {
-    for (int64_t p = P + threadIdx.x; p < 64; p += NT) pool[p] = 0ull;
-    __syncthreads();
-    if (threadIdx.x < 32) warp_sort64_desc(pool);
-    __syncthreads();
+    // P <= 64: every key counts the keys above it (broadcast smem reads;
+    // composite keys are unique) and writes itself at that rank — no sort
     pdl_wait_writes();
-    for (int64_t p = threadIdx.x; p < k; p += NT) emit_comp<DT>(pool[p], row * k + p, geo, out_vals, out_idx);
+    for (int p = threadIdx.x; p < (int)P; p += NT) {
+      const uint64_t x = pool[p];
+      if (!x) continue;  // empty slot
+      int f = 0;
+#pragma unroll 8
+      for (int j = 0; j < (int)P; ++j) f += pool[j] > x ? 1 : 0;
+      if (f < k) emit_comp<DT>(x, row * k + f, geo, out_vals, out_idx);
+    }
     return;
   }
   else {
