@@ -57,3 +57,42 @@ def test_error_strings_cover_codes():
     for s in range(0, 15):
         assert _lib.error_code(s) != "unknown"
         assert _lib.error_string(s)
+
+
+# (m, n, k, b, kb, dtype, fused?, launches per call) for the BASELINE configs
+_PLANS = [
+    (128, 65536, 64, 64, 1, _lib.BTK_F32, 1, 1),            # cfg1: cluster kernel
+    (128, 65536, 16384, 8192, 2, _lib.BTK_F32, 1, 1),       # cfg2: wide kernel
+    (128, 65536, 16384, 2048, 8, _lib.BTK_F32, 1, 1),
+    (128, 1 << 20, 256, 512, 1, _lib.BTK_BF16, 1, 1),       # cfg3
+    (4096, 32768, 512, 512, 1, _lib.BTK_BF16, 1, 1),        # cfg4: warp-per-row kernel
+    (8192, 1 << 20, 65536, 65536, 2, _lib.BTK_BF16, 0, 3),  # cfg5: stage 1 + select + LSD
+]
+
+
+@pytest.mark.parametrize("plan", _PLANS, ids=lambda p: f"m{p[0]}-n{p[1]}-k{p[2]}-b{p[3]}-kb{p[4]}")
+def test_launch_planner_host_side(plan):
+    """The host-side planner (no GPU needed) picks the fused single-launch
+    path for cfg1-4 and the generic multi-kernel path for cfg5, and sizes
+    the workspace for the generic path."""
+    m, n, k, b, kb, dt, fused, launches = plan
+    lib = _lib.load()
+    assert lib.btk_uses_fused_path(m, n, k, b, kb, dt, _lib.BTK_INTERLEAVED, n) == fused
+    assert lib.btk_launch_count(m, n, k, b, kb, dt, _lib.BTK_INTERLEAVED, n) == launches
+    # sized for the generic path too (the fused path's eligibility also
+    # depends on the input pointer's alignment, unknown here)
+    ws = lib.btk_workspace_bytes(m, n, k, b, kb, dt, _lib.BTK_INTERLEAVED)
+    assert ws >= (0 if fused else m * b * kb * 8)
+    # contiguous layout always takes the generic path
+    assert lib.btk_uses_fused_path(m, n, k, b, kb, dt, _lib.BTK_CONTIGUOUS, n) == 0
+    # a misaligned row stride (not 16-byte multiple) drops out of the fused envelope
+    assert lib.btk_uses_fused_path(m, n, k, b, kb, dt, _lib.BTK_INTERLEAVED, n + 1) == 0
+
+
+@pytest.mark.parametrize("s", ["1", "2", "4", "8"])
+def test_planner_cluster_overrides_stay_valid(s, monkeypatch):
+    monkeypatch.setenv("BTK_S", s)
+    monkeypatch.setenv("BTK_ROWS", "0")
+    lib = _lib.load()
+    for (m, n, k, b, kb, dt) in [(3, 65536, 64, 64, 1, _lib.BTK_F32), (2, 131072, 256, 1024, 1, _lib.BTK_BF16)]:
+        assert lib.btk_uses_fused_path(m, n, k, b, kb, dt, _lib.BTK_INTERLEAVED, n) == 1
