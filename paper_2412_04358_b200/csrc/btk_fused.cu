@@ -456,6 +456,69 @@ struct NarrowArgs {
   int trace;
 };
 
+// Tail shared by the cluster kernels: fold the R phase queues, push the
+// CTA's partial into the leader's slot (DSMEM store for crank > 0), one
+// cluster barrier, then the leader merges the S slots and runs Stage 2.
+template <int DT, int KB, int NT, int ITEMS>
+__device__ __forceinline__ void narrow_tail(const NarrowArgs& a, uint8_t* smem, Scanner<DT, KB>& sc,
+                                            bool active, int r, int g, int64_t t_begin,
+                                            uint32_t bad, int64_t row, int crank, bool tr,
+                                            cg::cluster_group& cluster) {
+  const int tid = threadIdx.x;
+  const int64_t b = a.b;
+  const int R = a.R;
+  uint64_t* scratch = reinterpret_cast<uint64_t*>(smem + a.scratch_off);
+  uint64_t* part = reinterpret_cast<uint64_t*>(smem + a.part_off);
+  uint64_t* pool = reinterpret_cast<uint64_t*>(smem + a.pool_off);
+  if (active) sc.template spill<KB>(scratch + (int64_t)r * b * KB, g, b, t_begin, a.geo);
+  __syncthreads();
+  // fold the R phase queues and push the CTA's partial straight into the
+  // leader's slot c (DSMEM store for c > 0): one cluster barrier, no remote
+  // reads
+  uint64_t* dst = (a.S > 1) ? cluster.map_shared_rank(part, 0) + (int64_t)crank * b * KB : part;
+  for (int64_t j = tid; j < b; j += NT) {
+    uint64_t best[KB];
+#pragma unroll
+    for (int z = 0; z < KB; ++z) best[z] = 0ull;
+    for (int rr = 0; rr < R; ++rr) {
+#pragma unroll
+      for (int z = 0; z < KB; ++z) comp_push<KB>(best, scratch[((int64_t)rr * b + j) * KB + z]);
+    }
+#pragma unroll
+    for (int z = 0; z < KB; ++z) dst[j * KB + z] = best[z];
+  }
+  const bool anybad = __syncthreads_or(bad);
+  if (anybad && tid == 0 && a.flag) atomicOr(a.flag, 1u);
+  if (a.S > 1) cluster.sync();  // all partials delivered to the leader
+  if (crank == 0) {
+    for (int64_t j = tid; j < b; j += NT) {
+      uint64_t best[KB];
+#pragma unroll
+      for (int z = 0; z < KB; ++z) best[z] = part[j * KB + z];
+      for (int c = 1; c < a.S; ++c) {
+#pragma unroll
+        for (int z = 0; z < KB; ++z) comp_push<KB>(best, part[((int64_t)c * b + j) * KB + z]);
+      }
+#pragma unroll
+      for (int z = 0; z < KB; ++z)
+        if (z < a.kb) pool[j * a.kb + z] = best[z];
+    }
+  }
+  if (tr) g_trace[blockIdx.x][3] = gtime();
+  if (crank != 0) {
+    if (tr) g_trace[blockIdx.x][4] = gtime();
+    return;
+  }
+  __syncthreads();
+  if (tr) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_trace[blockIdx.x][6] = smid;
+  }
+  stage2_emit<DT, NT, ITEMS>(pool, smem + a.aux_off, a.P, a.k, a.lognb, row, a.geo, a.out_vals,
+                            a.out_idx, a.trace != 0);
+  if (tr) g_trace[blockIdx.x][4] = gtime();}
+
 template <int DT, int KB, int NT, int ITEMS>
 __global__ void __launch_bounds__(NT) fused_narrow(NarrowArgs a) {
   constexpr int V = Vec<DT>::V;
@@ -552,59 +615,9 @@ __global__ void __launch_bounds__(NT) fused_narrow(NarrowArgs a) {
   const uint32_t bad = sc.nonfinite() ? 1u : 0u;
   if (tr) g_trace[blockIdx.x][2] = gtime();
 
-  // ---- phase queues -> smem (the ring is dead now)
-  uint64_t* scratch = reinterpret_cast<uint64_t*>(smem + a.scratch_off);
-  uint64_t* part = reinterpret_cast<uint64_t*>(smem + a.part_off);
-  uint64_t* pool = reinterpret_cast<uint64_t*>(smem + a.pool_off);
-  if (active) sc.template spill<KB>(scratch + (int64_t)r * b * KB, g, b, t_begin, a.geo);
-  __syncthreads();
-  // fold the R phase queues and push the CTA's partial straight into the
-  // leader's slot c (DSMEM store for c > 0): one cluster barrier, no remote
-  // reads
-  uint64_t* dst = (a.S > 1) ? cluster.map_shared_rank(part, 0) + (int64_t)crank * b * KB : part;
-  for (int64_t j = tid; j < b; j += NT) {
-    uint64_t best[KB];
-#pragma unroll
-    for (int z = 0; z < KB; ++z) best[z] = 0ull;
-    for (int rr = 0; rr < R; ++rr) {
-#pragma unroll
-      for (int z = 0; z < KB; ++z) comp_push<KB>(best, scratch[((int64_t)rr * b + j) * KB + z]);
-    }
-#pragma unroll
-    for (int z = 0; z < KB; ++z) dst[j * KB + z] = best[z];
-  }
-  const bool anybad = __syncthreads_or(bad);
-  if (anybad && tid == 0 && a.flag) atomicOr(a.flag, 1u);
-  if (a.S > 1) cluster.sync();  // all partials delivered to the leader
-  if (crank == 0) {
-    for (int64_t j = tid; j < b; j += NT) {
-      uint64_t best[KB];
-#pragma unroll
-      for (int z = 0; z < KB; ++z) best[z] = part[j * KB + z];
-      for (int c = 1; c < a.S; ++c) {
-#pragma unroll
-        for (int z = 0; z < KB; ++z) comp_push<KB>(best, part[((int64_t)c * b + j) * KB + z]);
-      }
-#pragma unroll
-      for (int z = 0; z < KB; ++z)
-        if (z < a.kb) pool[j * a.kb + z] = best[z];
-    }
-  }
-  if (tr) g_trace[blockIdx.x][3] = gtime();
-  if (crank != 0) {
-    if (tr) g_trace[blockIdx.x][4] = gtime();
-    return;
-  }
-  __syncthreads();
-  if (tr) {
-    uint32_t smid;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    g_trace[blockIdx.x][6] = smid;
-  }
-  stage2_emit<DT, NT, ITEMS>(pool, smem + a.aux_off, a.P, a.k, a.lognb, row, a.geo, a.out_vals,
-                            a.out_idx, a.trace != 0);
-  if (tr) g_trace[blockIdx.x][4] = gtime();
+  narrow_tail<DT, KB, NT, ITEMS>(a, smem, sc, active, r, g, t_begin, bad, row, crank, tr, cluster);
 }
+
 
 // ============================================================ rows (one warp per row)
 // Many short rows (cfg4: 4096 x 32768, b = 512): block-level barriers and
