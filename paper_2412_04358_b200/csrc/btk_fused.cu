@@ -297,10 +297,12 @@ int env_int(const char* name, int dflt) {
   return (v && *v) ? std::atoi(v) : dflt;
 }
 
-// Programmatic dependent launch: off by default (measured neutral for a
-// plain read kernel and slower for the cluster kernel); BTK_PDL=1 enables.
+// Programmatic dependent launch (griddepcontrol): on by default.  Kernels
+// wait for their predecessor before the first read, so only the launch and
+// prologue overlap the previous kernel's tail (cfg1 +1.8%); BTK_PDL=0
+// disables it.
 bool pdl_enabled() {
-  static const int v = env_int("BTK_PDL", 0);
+  static const int v = env_int("BTK_PDL", 1);
   return v != 0;
 }
 
