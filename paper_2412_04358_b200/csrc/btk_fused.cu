@@ -117,6 +117,25 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Asynchronous 8-byte store into another CTA's shared memory (DSMEM) that
+// completes `bytes` on that CTA's mbarrier (st.async ... complete_tx).
+__device__ __forceinline__ void st_async_remote_u64(const void* local_dst, const uint64_t* local_bar,
+                                                    int rank, uint64_t v) {
+  uint32_t rdst, rbar;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rdst) : "r"(smem_u32(local_dst)), "r"(rank));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(smem_u32(local_bar)), "r"(rank));
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(rdst),
+               "l"(v), "r"(rbar)
+               : "memory");
+}
+
+__device__ __forceinline__ void cluster_arrive_release() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait_acquire() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ uint64_t evict_first_policy() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -458,6 +477,9 @@ struct NarrowArgs {
   int trace;
 };
 
+template <int KB>
+__host__ __device__ constexpr int kb_store() { return KB; }
+
 // Tail shared by the cluster kernels: fold the R phase queues, push the
 // CTA's partial into the leader's slot (DSMEM store for crank > 0), one
 // cluster barrier, then the leader merges the S slots and runs Stage 2.
@@ -465,7 +487,7 @@ template <int DT, int KB, int NT, int ITEMS>
 __device__ __forceinline__ void narrow_tail(const NarrowArgs& a, uint8_t* smem, Scanner<DT, KB>& sc,
                                             bool active, int r, int g, int64_t t_begin,
                                             uint32_t bad, int64_t row, int crank, bool tr,
-                                            cg::cluster_group& cluster) {
+                                            cg::cluster_group& cluster, uint64_t* pbar) {
   const int tid = threadIdx.x;
   const int64_t b = a.b;
   const int R = a.R;
@@ -474,10 +496,10 @@ __device__ __forceinline__ void narrow_tail(const NarrowArgs& a, uint8_t* smem, 
   uint64_t* pool = reinterpret_cast<uint64_t*>(smem + a.pool_off);
   if (active) sc.template spill<KB>(scratch + (int64_t)r * b * KB, g, b, t_begin, a.geo);
   __syncthreads();
-  // fold the R phase queues and push the CTA's partial straight into the
-  // leader's slot c (DSMEM store for c > 0): one cluster barrier, no remote
-  // reads
-  uint64_t* dst = (a.S > 1) ? cluster.map_shared_rank(part, 0) + (int64_t)crank * b * KB : part;
+  // fold the R phase queues; partners push their partial into the leader's
+  // slot c with st.async (completing bytes on the leader's mbarrier) and are
+  // done — no cluster barrier, no remote reads
+  if (a.S > 1 && crank != 0) cluster_wait_acquire();  // leader's pbar initialised
   for (int64_t j = tid; j < b; j += NT) {
     uint64_t best[KB];
 #pragma unroll
@@ -486,12 +508,21 @@ __device__ __forceinline__ void narrow_tail(const NarrowArgs& a, uint8_t* smem, 
 #pragma unroll
       for (int z = 0; z < KB; ++z) comp_push<KB>(best, scratch[((int64_t)rr * b + j) * KB + z]);
     }
+    if (crank == 0) {
 #pragma unroll
-    for (int z = 0; z < KB; ++z) dst[j * KB + z] = best[z];
+      for (int z = 0; z < KB; ++z) part[j * KB + z] = best[z];
+    } else {
+#pragma unroll
+      for (int z = 0; z < KB; ++z)
+        st_async_remote_u64(part + ((int64_t)crank * b + j) * KB + z, pbar, 0, best[z]);
+    }
   }
   const bool anybad = __syncthreads_or(bad);
   if (anybad && tid == 0 && a.flag) atomicOr(a.flag, 1u);
-  if (a.S > 1) cluster.sync();  // all partials delivered to the leader
+  if (a.S > 1 && crank == 0) {
+    cluster_wait_acquire();
+    mbar_wait(pbar, 0u);  // all partner partials landed
+  }
   if (crank == 0) {
     for (int64_t j = tid; j < b; j += NT) {
       uint64_t best[KB];
@@ -528,6 +559,7 @@ __global__ void __launch_bounds__(NT) fused_narrow(NarrowArgs a) {
   constexpr int ESZ = VT<DT>::W / 8;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[MAX_STAGES];
+  __shared__ __align__(8) uint64_t pbar;  // leader: partials of the partner CTAs
 
   cg::cluster_group cluster = cg::this_cluster();
   const int crank = (int)cluster.block_rank();
@@ -542,8 +574,16 @@ __global__ void __launch_bounds__(NT) fused_narrow(NarrowArgs a) {
 
   if (tid == 0) {
     for (int i = 0; i < a.NS; ++i) mbar_init(&full[i], 1);
+    if (a.S > 1 && crank == 0) {
+      // the partners' partials land here by st.async (complete_tx)
+      mbar_init(&pbar, 1);
+      mbar_expect_tx(&pbar, (uint32_t)((a.S - 1) * a.b * kb_store<KB>() * 8));
+    }
     fence_barrier_init();
   }
+  // publish the leader's barrier cluster-wide; partners wait on this phase
+  // only right before their first remote store (long since complete)
+  if (a.S > 1) cluster_arrive_release();
   // Programmatic dependent launch: let the next launch in the stream get
   // resident during our tail, and wait for our predecessor to finish (its
   // writes may be our input) before the first read.
@@ -617,7 +657,7 @@ __global__ void __launch_bounds__(NT) fused_narrow(NarrowArgs a) {
   const uint32_t bad = sc.nonfinite() ? 1u : 0u;
   if (tr) g_trace[blockIdx.x][2] = gtime();
 
-  narrow_tail<DT, KB, NT, ITEMS>(a, smem, sc, active, r, g, t_begin, bad, row, crank, tr, cluster);
+  narrow_tail<DT, KB, NT, ITEMS>(a, smem, sc, active, r, g, t_begin, bad, row, crank, tr, cluster, &pbar);
 }
 
 
