@@ -1,4 +1,5 @@
-"""Per-CTA timeline of the narrow kernel (BTK_TRACE=1) for one launch in a
+"""Per-CTA timeline of the narrow/wide kernels (BTK_TRACE=1; fp32 configs:
+the trace buffer lives in the fp32 translation unit) for one launch in a
 stream of back-to-back launches.  Prints percentiles relative to the
 earliest CTA start."""
 import ctypes, os, sys
