@@ -311,3 +311,54 @@ def test_graph_replay_with_pdl_matches_eager(cfg):
     got_v, got_i = op.values.clone(), op.indices.clone()
     want = btk.approx_topk(bufs[6 % 3], k, sch)
     assert torch.equal(got_i, want.indices) and torch.equal(got_v, want.values)
+
+
+def _canonical_properties(x, r, k, b, kb):
+    """Size-independent checks of one approx_topk result on the device:
+    values are the input bits at the indices, indices are distinct, rows
+    are in canonical order (value desc, index asc on ties), and the set is
+    exactly the top-k of the Stage-1 candidates (reference approx.py:245-282)."""
+    m = x.shape[0]
+    idx, val = r.indices, r.values
+    assert idx.shape == (m, k) and idx.dtype == torch.int64
+    assert torch.equal(torch.gather(x, 1, idx).view(torch.int16 if x.element_size() == 2 else torch.int32),
+                       val.view(torch.int16 if x.element_size() == 2 else torch.int32))
+    s = torch.sort(idx, dim=1).values
+    assert bool((s[:, 1:] != s[:, :-1]).all())
+    vf = val.float()
+    desc = vf[:, :-1] >= vf[:, 1:]
+    tie_ok = (vf[:, :-1] != vf[:, 1:]) | (idx[:, :-1] < idx[:, 1:])
+    assert bool(desc.all()) and bool(tie_ok.all())
+    # the selected set is the top-k of the Stage-1 survivors
+    c = btk.stage1(x, btk.BucketScheme(b, kb, I))
+    cv = c.values.float()
+    kth = vf[:, -1:]
+    n_above = (cv > kth).sum(dim=1)
+    n_at = (cv == kth).sum(dim=1)
+    assert bool((n_above <= k - 1).all()) and bool((n_above + n_at >= k).all())
+
+
+@pytest.mark.parametrize("name", ["cfg2_kb2", "cfg3_r2", "cfg5"])
+def test_full_size_properties_and_row_subset(name):
+    """BASELINE sizes (cfg5: 8192 x 2^20 bf16, 17 GB in HBM): canonical
+    properties on every row on the device, exact oracle parity on a seeded
+    subset of rows (the CPU oracle cannot hold cfg5 as float64)."""
+    from bench import CONFIGS
+    dt_s, m, n, k, b, kb, _, _ = CONFIGS[name]
+    dt = DT[dt_s]
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = torch.empty((m, n), dtype=dt, device="cuda")
+    for r0 in range(0, m, 512):  # generate in slabs (fp32 temporaries stay small)
+        r1 = min(m, r0 + 512)
+        x[r0:r1] = torch.randn((r1 - r0, n), generator=g, device="cuda").to(dt)
+    r = btk.approx_topk(x, k, btk.BucketScheme(b, kb, I))
+    torch.cuda.synchronize()
+    _canonical_properties(x, r, k, b, kb)
+    rows = torch.randperm(m, generator=torch.Generator().manual_seed(5))[:3].tolist()
+    for row in rows:
+        x32 = x[row:row + 1].float().cpu().numpy()
+        wv, wi = O.approx_topk(x32, k, b, kb)
+        np.testing.assert_array_equal(r.indices[row:row + 1].cpu().numpy(), wi)
+        np.testing.assert_array_equal(_bits(r.values[row:row + 1]), _want_bits(wv, dt))
+    del x, r
+    torch.cuda.empty_cache()
