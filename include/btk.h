@@ -70,10 +70,16 @@ int btk_stage1_validate(int64_t n, int64_t b, int64_t kb);
  * reference core.py:155-158 (stage1_candidate_count). */
 int64_t btk_stage1_count(int64_t n, int64_t b, int64_t kb, int layout);
 
-/* Bytes of device workspace btk_approx_topk needs (0 is possible; the
- * fused kernels need none).  Contents need not be initialised. */
+/* Bytes of device workspace btk_approx_topk needs for ANY input pointer
+ * and row stride of this shape (the worst case; 0 is possible — the fused
+ * kernels need none).  Contents need not be initialised. */
 size_t btk_workspace_bytes(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, int dtype,
                            int layout);
+
+/* Bytes of workspace the plan for exactly this call (input pointer
+ * alignment and row stride included) needs: <= btk_workspace_bytes. */
+size_t btk_plan_workspace_bytes(const void* x, int64_t row_stride, int dtype, int64_t m, int64_t n,
+                                int64_t k, int64_t b, int64_t kb, int layout);
 
 /* Bucketed approximate top-k: Stage 1 (per-bucket top-k_b) + Stage 2 (exact
  * top-k over the survivors, canonical order).
@@ -114,6 +120,19 @@ int64_t btk_min_bytes(int64_t m, int64_t n, int64_t k, int64_t value_bytes, int6
 /* Which kernel family btk_approx_topk would run: 1 fused, 0 generic. */
 int btk_uses_fused_path(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, int dtype,
                         int layout, int64_t row_stride);
+
+/* Which kernel family btk_approx_topk runs for this problem (diagnostic;
+ * the tests assert every family is exercised).  -1 if invalid. */
+enum btk_family {
+  BTK_FAM_GENERIC = 0,     /* s1_generic (thread per bucket) + K2 */
+  BTK_FAM_NARROW = 1,      /* fused_narrow: TMA ring, cluster of S CTAs per row */
+  BTK_FAM_WIDE = 2,        /* fused_wide: one CTA per row, LDG vector columns */
+  BTK_FAM_ROWS = 3,        /* fused_rows: one warp per row */
+  BTK_FAM_VEC_POOL = 4,    /* s1_vec pool + K2 */
+  BTK_FAM_MATERIALIZE = 5  /* every element materialised + K2 (b == 1, k_b > 16) */
+};
+int btk_kernel_family(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, int dtype,
+                      int layout, int64_t row_stride);
 
 /* Number of kernel launches one btk_approx_topk call issues for this
  * problem (the bench's gpu_launches claim is derived from it). */

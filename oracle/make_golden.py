@@ -187,5 +187,29 @@ def main() -> None:
     print("golden fixtures written to", OUT)
 
 
+def cfg5_rows() -> None:
+    """cfg5 at m = 8 rows (b = 65536, k_b = 2, k = 65536 of n = 2^20, bf16
+    values): outputs stored as SHA-256 of the int64 indices and of the
+    float32 value bits (8 x 65536 pairs would be MBs of fixture), plus
+    row 0 in full for diagnosis."""
+    approx, core, _ = _ref()
+    m, n, k, b, kb, seed = 8, 1 << 20, 65536, 65536, 2, 112
+    x = gen_input("normal_bf16", m, n, seed)
+    r = approx.approx_topk(x, k, core.BucketScheme(b=b, k_b=kb, assignment=core.Assignment.INTERLEAVED),
+                           workers=os.cpu_count() or 1)
+    idx = np.ascontiguousarray(r.indices, dtype=np.int64)
+    val = np.ascontiguousarray(r.values, dtype=np.float32)
+    np.savez_compressed(os.path.join(OUT, "cfg5_rows.npz"), meta=np.array([m, n, k, b, kb, seed], np.int64),
+                        kind=np.array("normal_bf16"), sha=np.array(sha(x)),
+                        sha_indices=np.array(hashlib.sha256(idx.tobytes()).hexdigest()),
+                        sha_values=np.array(hashlib.sha256(val.tobytes()).hexdigest()),
+                        row0_indices=idx[0].astype(np.int32), row0_values=val[0])
+    print("cfg5_rows done", flush=True)
+
+
 if __name__ == "__main__":
-    main()
+    if "--cfg5" in sys.argv:
+        cfg5_rows()
+    else:
+        main()
+        cfg5_rows()

@@ -26,6 +26,7 @@ SIGNATURES = {
     "btk_stage1_validate": (_i, [_i64] * 3),
     "btk_stage1_count": (_i64, [_i64, _i64, _i64, _i]),
     "btk_workspace_bytes": (_sz, [_i64] * 5 + [_i, _i]),
+    "btk_plan_workspace_bytes": (_sz, [_vp, _i64, _i] + [_i64] * 5 + [_i]),
     "btk_approx_topk": (_i, [_vp, _i64, _i] + [_i64] * 5 + [_i, _vp, _vp, _vp, _sz, _vp, _vp]),
     "btk_stage1_workspace_bytes": (_sz, [_i64] * 4 + [_i, _i]),
     "btk_stage1": (_i, [_vp, _i64, _i] + [_i64] * 4 + [_i, _vp, _vp, _vp, _sz, _vp, _vp]),
@@ -36,6 +37,7 @@ SIGNATURES = {
     "btk_min_bytes": (_i64, [_i64] * 5),
     "btk_uses_fused_path": (_i, [_i64] * 5 + [_i, _i, _i64]),
     "btk_launch_count": (_i, [_i64] * 5 + [_i, _i, _i64]),
+    "btk_kernel_family": (_i, [_i64] * 5 + [_i, _i, _i64]),
     "btk_error_code": (ctypes.c_char_p, [_i]),
     "btk_error_string": (ctypes.c_char_p, [_i]),
     "btk_last_cuda_error": (_i, []),

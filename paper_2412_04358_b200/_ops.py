@@ -60,6 +60,11 @@ def to_device_tensor(scores, device=None) -> torch.Tensor:
     return t
 
 
+def host_array(scores) -> np.ndarray:
+    """Array-like -> NumPy array (no dtype change)."""
+    return np.asarray(scores)
+
+
 def as_rows(t: torch.Tensor, dim: int = -1):
     """(m, n) row view with unit inner stride, plus the leading shape.
 
@@ -97,8 +102,27 @@ def stream_handle(device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
-def check_flag(flag: torch.Tensor) -> None:
+_FLAGS = {}
+
+
+def device_flag(device) -> torch.Tensor:
+    """Non-finite flag per (device, current stream): int32, zero between
+    calls (check_flag resets it when it reads a set bit).  Calls on one
+    stream are ordered, and each reads its own launch's flag before the
+    next call is issued, so the flag never carries a stale bit."""
+    dev = torch.device(device)
+    key = (dev, torch.cuda.current_stream(dev).cuda_stream)
+    f = _FLAGS.get(key)
+    if f is None:
+        f = torch.zeros(1, dtype=torch.int32, device=dev)
+        _FLAGS[key] = f
+    return f
+
+
+def check_flag(flag: torch.Tensor, reset: bool = False) -> None:
     v = int(flag.item())
+    if v and reset:
+        flag.zero_()
     if v & 1:
         raise NonFiniteInputError("scores contain NaN or infinity")
     if v & 2:

@@ -115,8 +115,11 @@ class ApproxTopK:
             self.values = torch.empty((m, k), dtype=dtype, device=self.device)
             self.indices = torch.empty((m, k), dtype=torch.int64, device=self.device)
             self.flag = torch.zeros(1, dtype=torch.int32, device=self.device)
-            self.ws_bytes = self.lib.btk_workspace_bytes(m, n, k, scheme.b, scheme.k_b, self.dt,
-                                                         self.layout)
+            # workspace of the plan that will run for 16-byte aligned inputs
+            # of this stride (the fused kernels need none); a misaligned
+            # input is rejected at launch rather than silently re-planned
+            self.ws_bytes = self.lib.btk_plan_workspace_bytes(
+                256, self.row_stride, self.dt, m, n, k, scheme.b, scheme.k_b, self.layout)
             self.ws = _ops.workspace(self.ws_bytes, self.device)
 
     @property
@@ -131,6 +134,9 @@ class ApproxTopK:
         if tuple(x.shape) != (self.m, self.n) or (self.m > 1 and x.stride(0) != self.row_stride):
             raise ValueError(f"input shape/stride {tuple(x.shape)}/{x.stride()} does not match "
                              f"prepared ({self.m}, {self.n}) stride {self.row_stride}")
+        if x.data_ptr() % 16:
+            raise ValueError("prepared ApproxTopK needs a 16-byte aligned input (use approx_topk "
+                             "for arbitrary views)")
         st = self.lib.btk_approx_topk(
             x.data_ptr(), self.row_stride, self.dt, self.m, self.n, self.k, self.scheme.b,
             self.scheme.k_b, self.layout, self.values.data_ptr(), self.indices.data_ptr(),
@@ -143,18 +149,26 @@ class ApproxTopK:
         return TopKResult(values=self.values, indices=self.indices)
 
     def check_finite(self) -> None:
-        _ops.check_flag(self.flag)
+        """Raise NonFiniteInputError if any launch since the last check saw
+        NaN/inf (one device->host sync).  The flag is cleared on read, so
+        each check covers the launches after the previous one."""
+        _ops.check_flag(self.flag, reset=True)
 
 
 def approx_topk(scores, k: int, scheme: BucketScheme, mode: ExecutionMode = PerBucket(),
                 workers: int = 1, *, dim: int = -1, check_finite: bool = True,
                 devices: Optional[Sequence] = None) -> TopKResult:
-    """Bucketed approximate top-k (GPU).  See module docstring."""
+    """Bucketed approximate top-k (GPU).  See module docstring.
+
+    One kernel launch on the fused path (plus, when ``check_finite``, one
+    4-byte device->host read of the non-finite flag); outputs are fresh
+    tensors from the caching allocator, the workspace (generic path only)
+    too."""
     _check_mode(mode)
     if devices is not None and len(devices) > 1:
         from .shard import approx_topk_sharded
         return approx_topk_sharded(scores, k, scheme, devices=devices, dim=dim,
-                                   check_finite=check_finite)
+                                   check_finite=check_finite, gather=True)
     del workers
     dev0 = devices[0] if devices else None
     t = _ops.to_device_tensor(scores, dev0)
@@ -162,13 +176,36 @@ def approx_topk(scores, k: int, scheme: BucketScheme, mode: ExecutionMode = PerB
     x, lead = _ops.as_rows(t, dim)
     m, n = x.shape
     check_parameters(m, n, k, scheme.b, scheme.k_b)
-    with torch.cuda.device(x.device):
-        op = ApproxTopK(m, n, k, scheme, dtype=x.dtype, device=x.device, row_stride=x.stride(0))
-        op.launch(x)
-        if check_finite:
-            op.check_finite()
-    return TopKResult(values=_restore(op.values, lead, dim, orig_ndim),
-                      indices=_restore(op.indices, lead, dim, orig_ndim))
+    vals, idx, flag = _launch(x, k, scheme, check_finite)
+    if flag is not None:
+        with torch.cuda.device(x.device):
+            _ops.check_flag(flag, reset=True)
+    return TopKResult(values=_restore(vals, lead, dim, orig_ndim),
+                      indices=_restore(idx, lead, dim, orig_ndim))
+
+
+def _launch(x: torch.Tensor, k: int, scheme: BucketScheme, check_finite: bool):
+    """Asynchronous launch on x's device / current stream: fresh (m, k)
+    outputs, no host sync.  Returns (values, indices, flag or None)."""
+    m, n = x.shape
+    lib = _lib.load()
+    dt = _ops.dtype_code(x)
+    lay = _layout(scheme.assignment)
+    dev = x.device
+    with torch.cuda.device(dev):
+        vals = torch.empty((m, k), dtype=x.dtype, device=dev)
+        idx = torch.empty((m, k), dtype=torch.int64, device=dev)
+        wsb = lib.btk_plan_workspace_bytes(x.data_ptr(), x.stride(0), dt, m, n, k, scheme.b,
+                                           scheme.k_b, lay)
+        ws = _ops.workspace(wsb, dev) if wsb else None
+        flag = _ops.device_flag(dev) if check_finite else None
+        st = lib.btk_approx_topk(x.data_ptr(), x.stride(0), dt, m, n, k, scheme.b, scheme.k_b,
+                                 lay, vals.data_ptr(), idx.data_ptr(),
+                                 ws.data_ptr() if ws is not None else None, wsb,
+                                 flag.data_ptr() if flag is not None else None,
+                                 _ops.stream_handle(dev))
+        _ops.raise_status(st, "(approx_topk)")
+    return vals, idx, flag
 
 
 def stage1(scores, scheme: BucketScheme, mode: ExecutionMode = PerBucket(), *,

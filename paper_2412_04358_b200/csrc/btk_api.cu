@@ -142,6 +142,20 @@ size_t btk_workspace_bytes(int64_t m, int64_t n, int64_t k, int64_t b, int64_t k
   return std::max(plan_generic(m, n, k, b, kb).total(), fused_workspace_bytes(p));
 }
 
+size_t btk_plan_workspace_bytes(const void* x, int64_t row_stride, int dtype, int64_t m, int64_t n,
+                                int64_t k, int64_t b, int64_t kb, int layout) {
+  if (btk_validate(m, n, k, b, kb) != BTK_OK || !dtype_ok(dtype)) return 0;
+  Problem p{};
+  p.x = x;
+  p.row_stride = row_stride;
+  p.dtype = dtype;
+  p.m = m; p.n = n; p.k = k; p.b = b; p.kb = kb;
+  p.layout = layout;
+  p.geo = geo_for(dtype, n);
+  if (fused_supported(p)) return fused_workspace_bytes(p);
+  return plan_generic(m, n, k, b, kb).total();
+}
+
 int btk_uses_fused_path(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, int dtype,
                         int layout, int64_t row_stride) {
   if (btk_validate(m, n, k, b, kb) != BTK_OK || !dtype_ok(dtype)) return 0;
@@ -153,6 +167,22 @@ int btk_uses_fused_path(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, 
   p.layout = layout;
   p.geo = geo_for(dtype, n);
   return fused_supported(p) ? 1 : 0;
+}
+
+int btk_kernel_family(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, int dtype,
+                      int layout, int64_t row_stride) {
+  if (btk_validate(m, n, k, b, kb) != BTK_OK || !dtype_ok(dtype)) return -1;
+  Problem p{};
+  p.x = reinterpret_cast<const void*>(uintptr_t(256));
+  p.row_stride = row_stride;
+  p.dtype = dtype;
+  p.m = m; p.n = n; p.k = k; p.b = b; p.kb = kb;
+  p.layout = layout;
+  p.geo = geo_for(dtype, n);
+  const int fk = fused_kind(p);
+  if (fk) return fk;  // BTK_FAM_NARROW / WIDE / ROWS
+  if (b == 1 || kb > 16) return BTK_FAM_MATERIALIZE;
+  return stage1_vec_supported(p) ? BTK_FAM_VEC_POOL : BTK_FAM_GENERIC;
 }
 
 int btk_launch_count(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, int dtype,

@@ -16,6 +16,11 @@ bool fused_supported(const Problem& p) {
   return make_plan(p, pl);
 }
 
+int fused_kind(const Problem& p) {
+  Plan pl;
+  return make_plan(p, pl) ? (int)pl.kind : 0;
+}
+
 bool stage1_vec_supported(const Problem& p) {
   const int V = vec_of(p.dtype), esz = esz_of(p.dtype);
   if (p.layout != 0 || p.kb != kb_tmpl(p.kb) || V * p.kb > 16) return false;

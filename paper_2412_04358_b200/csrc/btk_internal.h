@@ -82,6 +82,8 @@ cudaError_t run_stage1_emit(const Problem& p, const uint64_t* pool, int64_t C, v
 cudaError_t run_fused(const Problem& p, void* out_vals, int64_t* out_idx, void* ws, size_t ws_bytes,
                       cudaStream_t st);
 bool fused_supported(const Problem& p);
+// Fused kernel the planner picks: 0 none, 1 narrow, 2 wide, 3 rows.
+int fused_kind(const Problem& p);
 size_t fused_workspace_bytes(const Problem& p);
 
 }  // namespace btk

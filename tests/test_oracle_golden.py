@@ -75,3 +75,16 @@ def test_oracle_baseline_shapes(case):
 def test_bytes_moved_known_answer():
     # reference test_bench.py:81-88
     assert O.bytes_moved(128, 2**20, 64, 4, 8) == 536_969_216
+
+
+def test_oracle_cfg5_rows_golden():
+    """cfg5 (b = 65536, k_b = 2, k = 65536 of 2^20) at m = 8, hashed outputs."""
+    from tests.golden_io import cfg5_rows, sha_bytes
+
+    c = cfg5_rows()
+    x = c["gen"]()
+    assert sha(x) == c["sha"]
+    v, i = O.approx_topk(x, c["k"], c["b"], c["kb"], workers=os.cpu_count() or 1)
+    np.testing.assert_array_equal(i[0], c["row0_indices"])
+    assert sha_bytes(i.astype(np.int64)) == c["sha_indices"]
+    assert sha_bytes(v.astype(np.float32)) == c["sha_values"]
