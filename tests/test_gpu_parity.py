@@ -228,12 +228,23 @@ def test_full_config4():
 
 def test_sharded_equals_single():
     rng = np.random.default_rng(9)
-    x = torch.from_numpy(rng.standard_normal((23, 4096), dtype=np.float32)).cuda()
+    x32 = rng.standard_normal((23, 4096), dtype=np.float32)
+    x = torch.from_numpy(x32).cuda()
     sch = btk.BucketScheme(256, 2, I)
     base = btk.approx_topk(x, 256, sch)
     devs = ["cuda:0"] * 3  # same device three times: exercises the partition logic
-    r = btk.approx_topk_sharded(x, 256, sch, devices=devs)
+    r = btk.approx_topk_sharded(x, 256, sch, devices=devs, gather=True)
     assert torch.equal(r.indices, base.indices) and torch.equal(r.values, base.values)
+    # default: results stay on the owning devices, one block per device
+    parts = btk.approx_topk_sharded(x32, 256, sch, devices=devs)  # host input, copied per block
+    assert [p.m for p in parts] == [s.stop - s.start for s in btk.row_blocks(23, 3)]
+    assert torch.equal(torch.cat([p.indices for p in parts]), base.indices)
+    # N-D input with dim != -1: gathered result has the single-device shape
+    x3 = torch.from_numpy(rng.standard_normal((3, 4096, 5), dtype=np.float32)).cuda()
+    one = btk.approx_topk(x3, 256, sch, dim=1)
+    many = btk.approx_topk(x3, 256, sch, dim=1, devices=devs)
+    assert many.values.shape == one.values.shape == (3, 256, 5)
+    assert torch.equal(many.indices, one.indices) and torch.equal(many.values, one.values)
 
 
 _SHAPE_ENVS = [{"BTK_ROWS": "1"}, {"BTK_ROWS": "0", "BTK_S": "1"}, {"BTK_ROWS": "0", "BTK_S": "2"},
