@@ -15,7 +15,7 @@
  *     void* (NULL = legacy default stream).  Calls are asynchronous and
  *     stream-ordered; the library never allocates, never synchronises.
  *   - Scores: m rows of n elements, row r at x + r*row_stride elements,
- *     unit stride inside a row.  dtype: BTK_F32 / BTK_BF16 / BTK_F16.
+ *     unit stride inside a row.  dtype: BTK_F32 / BTK_BF16 / BTK_F16 / BTK_F64.
  *   - Outputs are canonical: per row, value descending, ties by lower
  *     original index (reference exact.py:130-139); values are bit-exact
  *     copies of the selected inputs (sign of zero kept); indices int64.
@@ -36,7 +36,9 @@
 extern "C" {
 #endif
 
-enum btk_dtype { BTK_F32 = 0, BTK_BF16 = 1, BTK_F16 = 2 };
+/* BTK_F64: the reference's native dtype (exact.py:87-96 computes in
+ * float64); exact, on a generic 128-bit-key path (btk_f64.cu). */
+enum btk_dtype { BTK_F32 = 0, BTK_BF16 = 1, BTK_F16 = 2, BTK_F64 = 3 };
 
 /* reference core.py:28-47 (Assignment) */
 enum btk_layout { BTK_INTERLEAVED = 0, BTK_CONTIGUOUS = 1 };
@@ -129,7 +131,8 @@ enum btk_family {
   BTK_FAM_WIDE = 2,        /* fused_wide: one CTA per row, LDG vector columns */
   BTK_FAM_ROWS = 3,        /* fused_rows: one warp per row */
   BTK_FAM_VEC_POOL = 4,    /* s1_vec pool + K2 */
-  BTK_FAM_MATERIALIZE = 5  /* every element materialised + K2 (b == 1, k_b > 16) */
+  BTK_FAM_MATERIALIZE = 5, /* every element materialised + K2 (b == 1, k_b > 16) */
+  BTK_FAM_F64 = 6          /* float64: 128-bit keys (btk_f64.cu) */
 };
 int btk_kernel_family(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, int dtype,
                       int layout, int64_t row_stride);

@@ -207,9 +207,71 @@ def cfg5_rows() -> None:
     print("cfg5_rows done", flush=True)
 
 
+def philox_normal_rows(seed: int, first_row: int, rows: int, n: int) -> np.ndarray:
+    """Restatement of the reference's keyed generator (simdata.py:38-66):
+    row r is standard_normal(n) from Philox keyed (seed << 64) | (0 << 56) | r."""
+    out = np.empty((rows, n), dtype=np.float64)
+    for r in range(rows):
+        out[r] = np.random.Generator(np.random.Philox(key=(seed << 64) | (first_row + r))).standard_normal(n)
+    return out
+
+
+# float64 cases on the reference's own inputs (simdata.iid_normal): name,
+# m, n, k, b, kb, assignment, seed
+F64_CASES = [
+    ("f64_cfg1like", 16, 4096, 64, 64, 1, "interleaved", 201),
+    ("f64_kb2", 8, 65536, 512, 512, 2, "interleaved", 202),
+    ("f64_contig_kb4", 8, 10000, 100, 50, 4, "contiguous", 203),
+    ("f64_kb30", 4, 20000, 300, 10, 30, "interleaved", 204),
+    ("f64_ragged", 6, 10007, 333, 97, 5, "interleaved", 205),
+    ("f64_bigpool", 2, 131072, 12000, 8192, 2, "interleaved", 206),
+    ("f64_exact_b1", 4, 20000, 500, 1, 500, "interleaved", 207),
+    ("f64_exact_long", 2, 50000, 9000, 1, 9000, "contiguous", 208),
+]
+
+
+def f64_cases() -> None:
+    """Reference outputs on its own float64 generator (simdata.iid_normal):
+    approx_topk, stage1 and exact_topk_oracle, stored in full."""
+    approx, core, exact = _ref()
+    import bucketed_topk.simdata as simdata
+    out = {}
+    for name, m, n, k, b, kb, asg, seed in F64_CASES:
+        x = simdata.iid_normal(m, n, seed=seed)
+        assert np.array_equal(x, philox_normal_rows(seed, 0, m, n))
+        A = core.Assignment.INTERLEAVED if asg == "interleaved" else core.Assignment.CONTIGUOUS
+        scheme = core.BucketScheme(b=b, k_b=kb, assignment=A)
+        r = approx.approx_topk(x, k, scheme)
+        s1 = approx.stage1(x, scheme)
+        ex = exact.exact_topk_oracle(x, k)
+        out[f"{name}/meta"] = np.array([m, n, k, b, kb, seed], np.int64)
+        out[f"{name}/asg"] = np.array(asg)
+        out[f"{name}/sha"] = np.array(hashlib.sha256(x.tobytes()).hexdigest())
+        out[f"{name}/values"] = r.values
+        out[f"{name}/indices"] = r.indices
+        out[f"{name}/s1_values"] = s1.values
+        out[f"{name}/s1_indices"] = s1.indices
+        out[f"{name}/ex_values"] = ex.values
+        out[f"{name}/ex_indices"] = ex.indices
+        print(name, "done", flush=True)
+    # carried labels in float64 with repeated labels and signed zeros
+    rng = np.random.default_rng(301)
+    v = rng.integers(-2, 3, size=(3, 5000)).astype(np.float64) * rng.choice([1.0, 0.5e-310], size=(3, 5000))
+    v[:, ::7] = -0.0
+    lab = rng.integers(0, 600, size=(3, 5000)).astype(np.int64)
+    t = exact.topk_with_indices(v, lab, 777)
+    out["labels/v"], out["labels/lab"], out["labels/k"] = v, lab, np.array(777)
+    out["labels/values"], out["labels/indices"] = t.values, t.indices
+    np.savez_compressed(os.path.join(OUT, "f64_iid.npz"), names=np.array([c[0] for c in F64_CASES]), **out)
+    print("f64 cases done", flush=True)
+
+
 if __name__ == "__main__":
     if "--cfg5" in sys.argv:
         cfg5_rows()
+    elif "--f64" in sys.argv:
+        f64_cases()
     else:
         main()
         cfg5_rows()
+        f64_cases()

@@ -1,9 +1,10 @@
 """Tensor plumbing between the Python API and the C ABI.
 
 torch supplies device memory, streams and the caching allocator; every
-compute step is a libbtk.so kernel.  Inputs must be CUDA tensors (or
-NumPy / CPU tensors, which are copied to the current CUDA device first —
-the reference's callers pass NumPy arrays).
+compute step is a libbtk.so kernel.  Inputs are CUDA tensors, or NumPy /
+CPU tensors / lists, which are copied to the current CUDA device first
+(the reference's callers pass NumPy float64 arrays: float64 has its own
+exact GPU path, nothing is rounded).
 """
 
 from __future__ import annotations
@@ -14,7 +15,8 @@ import torch
 from . import _lib
 from .core import ConfigError, NonFiniteInputError
 
-_DTYPES = {torch.float32: _lib.BTK_F32, torch.bfloat16: _lib.BTK_BF16, torch.float16: _lib.BTK_F16}
+_DTYPES = {torch.float32: _lib.BTK_F32, torch.bfloat16: _lib.BTK_BF16, torch.float16: _lib.BTK_F16,
+           torch.float64: _lib.BTK_F64}
 
 # status codes that correspond to reference ConfigError codes
 _CONFIG_CODES = {1, 2, 3, 4, 5, 6, 7, 8}
@@ -40,8 +42,8 @@ def dtype_code(t: torch.Tensor) -> int:
         return _DTYPES[t.dtype]
     except KeyError:
         raise TypeError(
-            f"unsupported dtype {t.dtype}: the B200 kernels take float32, bfloat16 or float16 "
-            "(float64 has no exact 64-bit composite key)") from None
+            f"unsupported dtype {t.dtype}: the B200 kernels take float32, bfloat16, float16 or "
+            "float64") from None
 
 
 def to_device_tensor(scores, device=None) -> torch.Tensor:
@@ -49,11 +51,7 @@ def to_device_tensor(scores, device=None) -> torch.Tensor:
     if isinstance(scores, torch.Tensor):
         t = scores
     else:
-        a = np.asarray(scores)
-        if a.dtype == np.float64:
-            raise TypeError("float64 scores are not supported on the GPU path; pass float32, "
-                            "bfloat16 or float16 (exact upcasts of the same values)")
-        t = torch.from_numpy(np.ascontiguousarray(a))
+        t = torch.from_numpy(np.ascontiguousarray(host_array(scores)))
     if not t.is_cuda:
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         t = t.to(dev)
@@ -61,8 +59,13 @@ def to_device_tensor(scores, device=None) -> torch.Tensor:
 
 
 def host_array(scores) -> np.ndarray:
-    """Array-like -> NumPy array (no dtype change)."""
-    return np.asarray(scores)
+    """Array-like -> NumPy array.  NumPy float16/32/64 keep their dtype (each
+    has an exact GPU path); Python lists / ints / other dtypes become float64,
+    as the reference's _as_matrix does (exact.py:87-96)."""
+    a = np.asarray(scores)
+    if a.dtype not in (np.float16, np.float32, np.float64):
+        a = a.astype(np.float64)
+    return a
 
 
 def as_rows(t: torch.Tensor, dim: int = -1):

@@ -21,9 +21,9 @@ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 size_t al(size_t v) { return (v + 255) & ~(size_t)255; }
 
-bool dtype_ok(int d) { return d == BTK_F32 || d == BTK_BF16 || d == BTK_F16; }
+bool dtype_ok(int d) { return d == BTK_F32 || d == BTK_BF16 || d == BTK_F16 || d == BTK_F64; }
 
-int vbytes(int d) { return d == BTK_F32 ? 4 : 2; }
+int vbytes(int d) { return d == BTK_F64 ? 8 : (d == BTK_F32 ? 4 : 2); }
 
 CompGeo geo_for(int dtype, int64_t space) {
   switch (dtype) {
@@ -130,6 +130,7 @@ int64_t btk_stage1_count(int64_t n, int64_t b, int64_t kb, int layout) {
 size_t btk_workspace_bytes(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, int dtype,
                            int layout) {
   if (btk_validate(m, n, k, b, kb) != BTK_OK || !dtype_ok(dtype)) return 0;
+  if (dtype == BTK_F64) return f64_workspace_bytes(m, n, k, b, kb);
   // the fused plan depends on alignment only through x / row_stride; size it
   // for the aligned, contiguous case (the generic plan covers the rest)
   Problem p{};
@@ -145,6 +146,7 @@ size_t btk_workspace_bytes(int64_t m, int64_t n, int64_t k, int64_t b, int64_t k
 size_t btk_plan_workspace_bytes(const void* x, int64_t row_stride, int dtype, int64_t m, int64_t n,
                                 int64_t k, int64_t b, int64_t kb, int layout) {
   if (btk_validate(m, n, k, b, kb) != BTK_OK || !dtype_ok(dtype)) return 0;
+  if (dtype == BTK_F64) return f64_workspace_bytes(m, n, k, b, kb);
   Problem p{};
   p.x = x;
   p.row_stride = row_stride;
@@ -158,7 +160,7 @@ size_t btk_plan_workspace_bytes(const void* x, int64_t row_stride, int dtype, in
 
 int btk_uses_fused_path(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, int dtype,
                         int layout, int64_t row_stride) {
-  if (btk_validate(m, n, k, b, kb) != BTK_OK || !dtype_ok(dtype)) return 0;
+  if (btk_validate(m, n, k, b, kb) != BTK_OK || !dtype_ok(dtype) || dtype == BTK_F64) return 0;
   Problem p{};
   p.x = reinterpret_cast<const void*>(uintptr_t(256));
   p.row_stride = row_stride;
@@ -172,6 +174,7 @@ int btk_uses_fused_path(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, 
 int btk_kernel_family(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, int dtype,
                       int layout, int64_t row_stride) {
   if (btk_validate(m, n, k, b, kb) != BTK_OK || !dtype_ok(dtype)) return -1;
+  if (dtype == BTK_F64) return BTK_FAM_F64;
   Problem p{};
   p.x = reinterpret_cast<const void*>(uintptr_t(256));
   p.row_stride = row_stride;
@@ -189,6 +192,11 @@ int btk_launch_count(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, int
                      int layout, int64_t row_stride) {
   if (btk_validate(m, n, k, b, kb) != BTK_OK || !dtype_ok(dtype)) return 0;
   if (btk_uses_fused_path(m, n, k, b, kb, dtype, layout, row_stride)) return 1;
+  if (dtype == BTK_F64) {
+    auto segn = [](int64_t L, int64_t kk) { return L <= 8192 ? 1 : (kk <= 8192 ? 2 : 2); };
+    if (b == 1) return segn(n, k);
+    return (kb <= 16 ? 1 : segn(ceil_div(n, b), kb)) + segn(b * kb, k);
+  }
   auto k2n = [](int64_t L, int64_t kk) { return L <= K2_SMALL_CAP ? 1 : 2; };
   if (b == 1) return 1 + k2n(n, k);
   int c = (kb <= 16) ? 1 : 1 + k2n(ceil_div(n, b), kb);
@@ -204,6 +212,11 @@ int btk_approx_topk(const void* x, int64_t row_stride, int dtype, int64_t m, int
   if (rc) return rc;
   if (!out_vals || !out_idx) return BTK_ERR_SHAPE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == BTK_F64) {
+    const size_t need = f64_workspace_bytes(m, n, k, b, kb);
+    if (ws_bytes < need || (need && (reinterpret_cast<uintptr_t>(ws) & 255))) return BTK_ERR_WORKSPACE;
+    return cuda_status(f64_approx_topk(x, row_stride, m, n, k, b, kb, layout, out_vals, out_idx, ws, flag, st));
+  }
   Problem p{};
   p.x = x;
   p.row_stride = row_stride;
@@ -252,9 +265,9 @@ int btk_approx_topk(const void* x, int64_t row_stride, int dtype, int64_t m, int
 
 size_t btk_stage1_workspace_bytes(int64_t m, int64_t n, int64_t b, int64_t kb, int dtype,
                                   int layout) {
-  (void)dtype;
   (void)layout;
   if (btk_stage1_validate(n, b, kb) != BTK_OK || m < 1) return 0;
+  if (dtype == BTK_F64) return f64_stage1_workspace_bytes(m, n, b, kb);
   Plan pl = plan_generic(m, n, std::max<int64_t>(1, std::min<int64_t>(n, b * kb)), b, kb);
   pl.pool = (size_t)(m * b * kb * 8);
   pl.s2a = pl.s2b = 0;
@@ -276,6 +289,9 @@ int btk_stage1(const void* x, int64_t row_stride, int dtype, int64_t m, int64_t 
   const size_t need = btk_stage1_workspace_bytes(m, n, b, kb, dtype, layout);
   if (ws_bytes < need || (need && (reinterpret_cast<uintptr_t>(ws) & 255))) return BTK_ERR_WORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == BTK_F64)
+    return cuda_status(f64_stage1(x, row_stride, m, n, b, kb, layout, btk_stage1_count(n, b, kb, layout),
+                                  out_vals, out_idx, ws, flag, st));
   Problem p{};
   p.x = x; p.row_stride = row_stride; p.dtype = dtype;
   p.m = m; p.n = n; p.k = std::min<int64_t>(n, b * kb); p.b = b; p.kb = kb;
@@ -325,13 +341,29 @@ __global__ void label_comps(const void* __restrict__ vals, const int64_t* __rest
   const int b1 = __syncthreads_or(bad), b2 = __syncthreads_or(badlab);
   if (threadIdx.x == 0 && flag && (b1 || b2)) atomicOr(flag, (b1 ? 1u : 0u) | (b2 ? 2u : 0u));
 }
+
+__global__ void label_range(const int64_t* __restrict__ labels, int64_t total, uint32_t* flag) {
+  bool bad = false;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lab = labels[t];
+    bad |= (lab < 0) || (lab > 0x7FFFFFFF);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0 && flag) atomicOr(flag, 2u);
+}
+
+cudaError_t label_check(const int64_t* labels, int64_t total, uint32_t* flag, cudaStream_t st) {
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 16));
+  label_range<<<grid, 256, 0, st>>>(labels, total, flag);
+  return cudaGetLastError();
+}
 }  // namespace
 
 extern "C" {
 
 size_t btk_topk_with_indices_workspace_bytes(int64_t m, int64_t c, int64_t k, int dtype) {
-  (void)dtype;
   if (m < 1 || c < 1 || k < 1 || k > c) return 0;
+  if (dtype == BTK_F64) return f64_pairs_workspace_bytes(m, c, k);
   size_t v = al((size_t)(m * c * 8));
   if (c > K2_SMALL_CAP) v += 2 * al((size_t)(m * k * 8));
   return v;
@@ -347,6 +379,12 @@ int btk_topk_with_indices(const void* values, const int64_t* labels, int dtype, 
   const size_t need = btk_topk_with_indices_workspace_bytes(m, c, k, dtype);
   if (ws_bytes < need || (reinterpret_cast<uintptr_t>(ws) & 255)) return BTK_ERR_WORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == BTK_F64) {
+    if (c >= (int64_t(1) << 32)) return BTK_ERR_SHAPE;
+    int rc = cuda_status(label_check(labels, m * c, flag, st));
+    if (rc) return rc;
+    return cuda_status(f64_topk_with_indices(values, labels, m, c, k, out_vals, out_idx, ws, flag, st));
+  }
   const CompGeo g = geo_for(dtype, int64_t(1) << 31);
   Carve cv{static_cast<uint8_t*>(ws)};
   uint64_t* comps = cv.take((size_t)(m * c * 8));
@@ -405,7 +443,7 @@ const char* btk_error_string(int s) {
     case BTK_ERR_INSUFFICIENT_CANDIDATES: return "stage 1 yields fewer than k candidates";
     case BTK_ERR_CHUNKS_RANGE: return "chunks_per_bucket must be >= 2";
     case BTK_ERR_ASSIGNMENT: return "unknown assignment";
-    case BTK_ERR_DTYPE: return "unsupported dtype (float32, bfloat16, float16)";
+    case BTK_ERR_DTYPE: return "unsupported dtype (float32, bfloat16, float16, float64)";
     case BTK_ERR_SHAPE: return "scores must be a non-empty m x n matrix";
     case BTK_ERR_WORKSPACE: return "workspace too small or not 256-byte aligned";
     case BTK_ERR_ALIGNMENT: return "misaligned device pointer";

@@ -86,4 +86,18 @@ bool fused_supported(const Problem& p);
 int fused_kind(const Problem& p);
 size_t fused_workspace_bytes(const Problem& p);
 
+// Exact float64 path (btk_f64.cu): 128-bit composite keys.
+size_t f64_workspace_bytes(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb);
+size_t f64_stage1_workspace_bytes(int64_t m, int64_t n, int64_t b, int64_t kb);
+size_t f64_pairs_workspace_bytes(int64_t m, int64_t c, int64_t k);
+cudaError_t f64_approx_topk(const void* x, int64_t row_stride, int64_t m, int64_t n, int64_t k, int64_t b,
+                            int64_t kb, int layout, void* out_vals, int64_t* out_idx, void* ws,
+                            uint32_t* flag, cudaStream_t st);
+cudaError_t f64_stage1(const void* x, int64_t row_stride, int64_t m, int64_t n, int64_t b, int64_t kb,
+                       int layout, int64_t C, void* out_vals, int64_t* out_idx, void* ws, uint32_t* flag,
+                       cudaStream_t st);
+cudaError_t f64_topk_with_indices(const void* values, const int64_t* labels, int64_t m, int64_t c,
+                                  int64_t k, void* out_vals, int64_t* out_idx, void* ws, uint32_t* flag,
+                                  cudaStream_t st);
+
 }  // namespace btk

@@ -88,3 +88,24 @@ def test_oracle_cfg5_rows_golden():
     np.testing.assert_array_equal(i[0], c["row0_indices"])
     assert sha_bytes(i.astype(np.int64)) == c["sha_indices"]
     assert sha_bytes(v.astype(np.float32)) == c["sha_values"]
+
+
+def test_oracle_f64_iid_golden():
+    """The oracle on the reference's own float64 inputs (keyed Philox,
+    simdata.py:38-66) against the reference's outputs."""
+    import hashlib
+
+    from tests.golden_io import f64_cases, f64_labels
+
+    for c in f64_cases():
+        x = c["gen"]()
+        assert hashlib.sha256(x.tobytes()).hexdigest() == c["sha"], c["name"]
+        v, i = O.approx_topk(x, c["k"], c["b"], c["kb"], c["asg"])
+        assert np.array_equal(i, c["indices"]) and np.array_equal(v.view(np.int64), c["values"].view(np.int64))
+        sv, si, _ = O.stage1(x, c["b"], c["kb"], c["asg"])
+        assert np.array_equal(si, c["s1_indices"]) and np.array_equal(sv, c["s1_values"])
+        ev, ei = O.exact_topk(x, c["k"])
+        assert np.array_equal(ei, c["ex_indices"]) and np.array_equal(ev, c["ex_values"])
+    L = f64_labels()
+    v, i = O.topk_with_indices(L["v"], L["lab"], int(L["k"]))
+    assert np.array_equal(i, L["indices"]) and np.array_equal(v.view(np.int64), L["values"].view(np.int64))
