@@ -68,11 +68,11 @@ __device__ __forceinline__ uint32_t digit(const K128& k, int shift) {
   return shift >= 64 ? (uint32_t)(k.hi >> (shift - 64)) & 0xFFu : (uint32_t)(k.lo >> shift) & 0xFFu;
 }
 
-// Keys above bit `shift` (the MSD prefix), compared as 128-bit.
+// key >> shift as a 128-bit number (the MSD prefix), shift in [0, 128].
 __device__ __forceinline__ K128 prefix_of(const K128& k, int shift) {
   K128 r;
   if (shift >= 128) { r.hi = r.lo = 0; return r; }
-  if (shift >= 64) { r.hi = k.hi >> (shift - 64); r.lo = 0; return r; }
+  if (shift >= 64) { r.lo = k.hi >> (shift - 64); r.hi = 0; return r; }  // value of key >> shift
   if (shift == 0) return k;
   r.lo = (k.lo >> shift) | (k.hi << (64 - shift));
   r.hi = k.hi >> shift;
