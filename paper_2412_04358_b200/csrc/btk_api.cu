@@ -56,6 +56,18 @@ Plan plan_generic(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb) {
   return pl;
 }
 
+// The plan of one call: the chunked Stage 2 (btk_pool.cu) when the pool is
+// large and the vectorised Stage 1 applies, else plan_generic.
+Plan plan_for(const Problem& p) {
+  if (p.b > 1 && pool_chunked_ok(p)) {
+    Plan pl;
+    pl.pool = (size_t)(p.m * p.b * p.kb * 8);
+    pl.s2a = pool_chunked_bytes(p);  // hist | tab | chunk buffer (fallback scratch aliases it + the pool)
+    return pl;
+  }
+  return plan_generic(p.m, p.n, p.k, p.b, p.kb);
+}
+
 struct Carve {
   uint8_t* p;
   uint64_t* take(size_t bytes) {
@@ -140,7 +152,7 @@ size_t btk_workspace_bytes(int64_t m, int64_t n, int64_t k, int64_t b, int64_t k
   p.m = m; p.n = n; p.k = k; p.b = b; p.kb = kb;
   p.layout = layout;
   p.geo = geo_for(dtype, n);
-  return std::max(plan_generic(m, n, k, b, kb).total(), fused_workspace_bytes(p));
+  return std::max({plan_generic(m, n, k, b, kb).total(), plan_for(p).total(), fused_workspace_bytes(p)});
 }
 
 size_t btk_plan_workspace_bytes(const void* x, int64_t row_stride, int dtype, int64_t m, int64_t n,
@@ -155,7 +167,7 @@ size_t btk_plan_workspace_bytes(const void* x, int64_t row_stride, int dtype, in
   p.layout = layout;
   p.geo = geo_for(dtype, n);
   if (fused_supported(p)) return fused_workspace_bytes(p);
-  return plan_generic(m, n, k, b, kb).total();
+  return plan_for(p).total();
 }
 
 int btk_uses_fused_path(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, int dtype,
@@ -185,6 +197,7 @@ int btk_kernel_family(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, in
   const int fk = fused_kind(p);
   if (fk) return fk;  // BTK_FAM_NARROW / WIDE / ROWS
   if (b == 1 || kb > 16) return BTK_FAM_MATERIALIZE;
+  if (pool_chunked_ok(p)) return BTK_FAM_POOL_CHUNKED;
   return stage1_vec_supported(p) ? BTK_FAM_VEC_POOL : BTK_FAM_GENERIC;
 }
 
@@ -196,6 +209,14 @@ int btk_launch_count(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, int
     auto segn = [](int64_t L, int64_t kk) { return L <= 8192 ? 1 : (kk <= 8192 ? 2 : 2); };
     if (b == 1) return segn(n, k);
     return (kb <= 16 ? 1 : segn(ceil_div(n, b), kb)) + segn(b * kb, k);
+  }
+  {
+    Problem p{};
+    p.x = reinterpret_cast<const void*>(uintptr_t(256));
+    p.row_stride = row_stride; p.dtype = dtype;
+    p.m = m; p.n = n; p.k = k; p.b = b; p.kb = kb; p.layout = layout; p.geo = geo_for(dtype, n);
+    // s1_vec + pool_scatter + pool_sort + fallback (select/compact, sort); the memset is not a kernel
+    if (b > 1 && pool_chunked_ok(p)) return 3 + (k <= K2_SMALL_CAP ? 2 : 2);
   }
   auto k2n = [](int64_t L, int64_t kk) { return L <= K2_SMALL_CAP ? 1 : 2; };
   if (b == 1) return 1 + k2n(n, k);
@@ -231,10 +252,14 @@ int btk_approx_topk(const void* x, int64_t row_stride, int dtype, int64_t m, int
     return cuda_status(run_fused(p, out_vals, out_idx, ws, ws_bytes, st));
   }
 
-  const Plan pl = plan_generic(m, n, k, b, kb);
+  const Plan pl = plan_for(p);
   if (ws_bytes < pl.total() || (pl.total() && (reinterpret_cast<uintptr_t>(ws) & 255)))
     return BTK_ERR_WORKSPACE;
   Carve cv{static_cast<uint8_t*>(ws)};
+  if (b > 1 && pool_chunked_ok(p)) {
+    uint64_t* pool = cv.take(pl.pool);
+    return cuda_status(run_pool_chunked(p, pool, cv.p, out_vals, out_idx, st));
+  }
   if (b == 1) {
     // single bucket: Stage 1 is already the exact canonical top-k (k_b == k)
     uint64_t* mat = cv.take(pl.mat);

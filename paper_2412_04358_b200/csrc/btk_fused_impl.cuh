@@ -370,13 +370,19 @@ struct Scanner {
   template <int KBS>
   __device__ __forceinline__ void spill(uint64_t* dst, int g, int64_t b, int64_t t_begin,
                                         const CompGeo& geo) const {
+    each_comp(g, b, t_begin, geo, [&](int64_t col, int z, uint64_t c) { dst[col * KBS + z] = c; });
+  }
+  // f(col, z, comp) for the KB survivors of each of the V buckets (0 = empty)
+  template <class F>
+  __device__ __forceinline__ void each_comp(int g, int64_t b, int64_t t_begin, const CompGeo& geo,
+                                            F&& f) const {
 #pragma unroll
     for (int e = 0; e < V; ++e) {
       const int64_t col = (int64_t)g * V + e;
 #pragma unroll
       for (int z = 0; z < KB; ++z) {
         const int t = q[e].t[z] < 0 ? -1 : (int)(t_begin + q[e].t[z]);
-        dst[col * KBS + z] = comp_of<DT>(q[e].v[z], t, col, b, geo);
+        f(col, z, comp_of<DT>(q[e].v[z], t, col, b, geo));
       }
     }
   }
@@ -437,6 +443,15 @@ struct Scanner16x2 {
   template <int KBS>
   __device__ __forceinline__ void spill(uint64_t* dst, int g, int64_t b, int64_t t_begin,
                                         const CompGeo& geo) const {
+    each_comp(g, b, t_begin, geo, [&](int64_t col, int, uint64_t c) {
+      dst[col * KBS] = c;
+#pragma unroll
+      for (int z = 1; z < KBS; ++z) dst[col * KBS + z] = 0ull;
+    });
+  }
+  template <class F>
+  __device__ __forceinline__ void each_comp(int g, int64_t b, int64_t t_begin, const CompGeo& geo,
+                                            F&& f) const {
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
 #pragma unroll
@@ -449,9 +464,7 @@ struct Scanner16x2 {
           const int64_t idx = (t_begin + code) * b + col;
           c = make_comp(vkey<DT>(raw), (uint32_t)idx, is_negzero<DT>(raw), geo);
         }
-        dst[col * KBS] = c;
-#pragma unroll
-        for (int z = 1; z < KBS; ++z) dst[col * KBS + z] = 0ull;
+        f(col, 0, c);
       }
     }
   }
@@ -834,35 +847,62 @@ __global__ void __launch_bounds__(NT, 1) fused_wide(WideArgs a) {
 // per row).  Same per-thread vector-column scan as fused_wide, but one
 // thread per column across the whole grid and all of a column's slots in
 // flight at once; survivors go to pool[row][j*k_b + z] (btk_stage1.cu's
-// layout), the input to K2.
-template <int DT, int KB, int U>
+// layout), the input to K2.  HIST: also count the survivors per coarse
+// bin (the top POOL_HBITS bits of the composite key) in shared memory and
+// flush the CTA's counts to hist[row][bin] with global atomics — the
+// chunked Stage 2 (btk_pool.cu) plans from it without re-reading the pool.
+// A CTA covers `groups` consecutive 256-column groups of one row.
+template <int DT, int KB, int U, bool HIST>
 __global__ void __launch_bounds__(256) s1_vec(const void* __restrict__ x, int64_t row_stride,
                                               int64_t n, int64_t b, int64_t s, int64_t G,
                                               int last_vec, CompGeo geo,
-                                              uint64_t* __restrict__ pool, uint32_t* flag) {
+                                              uint64_t* __restrict__ pool, uint32_t* flag,
+                                              uint32_t* __restrict__ hist, int groups) {
   constexpr int V = Vec<DT>::V;
   constexpr int ESZ = VT<DT>::W / 8;
+  constexpr int NBINS = HIST ? (1 << POOL_HBITS) : 1;
+  __shared__ uint32_t sh[NBINS];
   const int64_t row = blockIdx.y;
-  const int64_t g = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const int hshift = geo.nbits - POOL_HBITS;
   uint32_t bad = 0;
-  if (g < G) {
-    const uint8_t* colp = static_cast<const uint8_t*>(x) + (row * row_stride + g * V) * ESZ;
-    const int64_t s_eff = (g < last_vec) ? s : s - 1;
-    Scanner<DT, KB> sc;
-    sc.init();
-    int64_t t0 = 0;
-    for (; t0 + U <= s_eff; t0 += U) {
-      uint4 v[U];
+  if constexpr (HIST) {
+    for (int i = threadIdx.x; i < NBINS; i += 256) sh[i] = 0u;
+    __syncthreads();
+  }
+  for (int grp = 0; grp < groups; ++grp) {
+    const int64_t g = ((int64_t)blockIdx.x * groups + grp) * 256 + threadIdx.x;
+    if (g < G) {
+      const uint8_t* colp = static_cast<const uint8_t*>(x) + (row * row_stride + g * V) * ESZ;
+      const int64_t s_eff = (g < last_vec) ? s : s - 1;
+      Scanner<DT, KB> sc;
+      sc.init();
+      int64_t t0 = 0;
+      for (; t0 + U <= s_eff; t0 += U) {
+        uint4 v[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) v[u] = ldg_stream(colp + (t0 + u) * b * ESZ);
+        for (int u = 0; u < U; ++u) v[u] = ldg_stream(colp + (t0 + u) * b * ESZ);
 #pragma unroll
-      for (int u = 0; u < U; ++u) sc.row(v[u], (int)(t0 + u));
+        for (int u = 0; u < U; ++u) sc.row(v[u], (int)(t0 + u));
+      }
+      for (; t0 < s_eff; ++t0) sc.row(ldg_stream(colp + t0 * b * ESZ), (int)t0);
+      bad |= sc.nonfinite() ? 1u : 0u;
+      uint64_t* dst = pool + row * b * KB;
+      if constexpr (HIST) {
+        sc.each_comp((int)g, b, 0, geo, [&](int64_t col, int z, uint64_t c) {
+          dst[col * KB + z] = c;
+          if (c) atomicAdd(&sh[(uint32_t)(c >> hshift)], 1u);
+        });
+      } else {
+        sc.template spill<KB>(dst, (int)g, b, 0, geo);
+      }
     }
-    for (; t0 < s_eff; ++t0) sc.row(ldg_stream(colp + t0 * b * ESZ), (int)t0);
-    bad = sc.nonfinite() ? 1u : 0u;
-    sc.template spill<KB>(pool + row * b * KB, (int)g, b, 0, geo);
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0 && flag) atomicOr(flag, 1u);
+  if constexpr (HIST) {
+    uint32_t* hr = hist + row * NBINS;
+    for (int i = threadIdx.x; i < NBINS; i += 256)
+      if (sh[i]) atomicAdd(&hr[i], sh[i]);
+  }
 }
 
 // ============================================================ planning

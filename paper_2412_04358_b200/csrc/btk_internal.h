@@ -13,6 +13,20 @@ namespace btk {
 // Longest segment K2 sorts entirely in one CTA's shared memory.
 constexpr int64_t K2_SMALL_CAP = 16384;
 
+// Chunked Stage 2 for large pools (btk_pool.cu): coarse bins = the top
+// POOL_HBITS bits of a composite key (8 bf16/fp16 values or 2^19 fp32
+// ulps per bin); chunks of whole bins start at multiples of POOL_HALF
+// selected keys, so a chunk holds < 2 * POOL_HALF keys when no selected
+// bin exceeds POOL_HALF (else the row takes the radix-select fallback).
+constexpr int POOL_HBITS = 13;
+constexpr int POOL_HALF = 8192;
+constexpr int POOL_MAXC = 16;  // chunks per row (k <= (POOL_MAXC - 1) * POOL_HALF)
+struct ChunkTab {
+  int n;                      // chunks (-1: this row takes the fallback)
+  int start[POOL_MAXC + 1];   // output offset of chunk c (= its offset in the chunk buffer)
+  int pad[2];
+};
+
 struct K2Args {
   const uint64_t* in;   // nseg segments of L keys (row stride in_stride)
   int64_t in_stride;
@@ -27,6 +41,12 @@ struct K2Args {
   uint64_t* scratch_a;  // long segments only: nseg * kk keys each
   uint64_t* scratch_b;
   bool unique = true;   // keys unique (false: repeated carried labels possible)
+  // optional row mask: segment s runs only if mask[s * mask_stride] < 0
+  // (the chunked Stage 2's fallback rows); scratch_b may use its own stride
+  const int* mask = nullptr;
+  int64_t mask_stride = 0;
+  int64_t scratch_a_stride = 0;  // 0: kk
+  int64_t scratch_b_stride = 0;  // 0: kk
 };
 
 // Opt a kernel into >48 KB dynamic smem once per device (never during
@@ -69,7 +89,13 @@ cudaError_t run_stage1_generic(const Problem& p, uint64_t* pool, cudaStream_t st
 // Vectorised stage 1 into the same pool (interleaved, k_b in {1,2,4,8},
 // V*k_b <= 16, 16-byte aligned rows); cudaErrorNotSupported otherwise.
 bool stage1_vec_supported(const Problem& p);
-cudaError_t run_stage1_vec(const Problem& p, uint64_t* pool, cudaStream_t st);
+cudaError_t run_stage1_vec(const Problem& p, uint64_t* pool, cudaStream_t st,
+                           uint32_t* hist = nullptr);
+// Chunked Stage 2 over a stage-1 pool with its coarse histogram.
+bool pool_chunked_ok(const Problem& p);
+size_t pool_chunked_bytes(const Problem& p);  // hist + tab + chunk buffer
+cudaError_t run_pool_chunked(const Problem& p, uint64_t* pool, void* ws, void* out_vals,
+                             int64_t* out_idx, cudaStream_t st);
 // All of a row's elements as comps, bucket-major (m*b segments of s slots).
 cudaError_t run_materialize(const Problem& p, uint64_t* mat, cudaStream_t st);
 // pool (m x b*kb) -> compact (m x C) values/indices in bucket order.

@@ -37,12 +37,14 @@ __global__ void __launch_bounds__(NT) k2_small(const uint64_t* __restrict__ in, 
                                                int64_t L, int64_t kk, uint64_t* __restrict__ out_keys,
                                                void* __restrict__ out_vals,
                                                int64_t* __restrict__ out_idx, int64_t out_stride,
-                                               CompGeo g, int lognb) {
+                                               CompGeo g, int lognb, const int* mask,
+                                               int64_t mask_stride) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw);
   uint8_t* aux = smem_raw + ((size_t)L * 8 + 127) / 128 * 128;
   const RankSmem S = rank_smem(sk, aux, L, kk, lognb, NT);
   const int64_t seg = blockIdx.x;
+  if (mask && mask[seg * mask_stride] >= 0) return;  // row handled by the chunked path
   const uint64_t* src = in + seg * in_stride;
   for (int p = threadIdx.x; p < L; p += NT) sk[p] = src[p];
   __syncthreads();
@@ -64,12 +66,14 @@ template <int NT>
 __global__ void __launch_bounds__(NT) k2_select_compact(const uint64_t* __restrict__ in,
                                                         int64_t in_stride, int64_t L, int64_t kk,
                                                         uint64_t* __restrict__ out,
-                                                        int64_t out_stride, int nbits) {
+                                                        int64_t out_stride, int nbits,
+                                                        const int* mask, int64_t mask_stride) {
   __shared__ uint32_t hist[RADIX];
   __shared__ int s_bin;
   __shared__ uint32_t s_above;
   __shared__ uint32_t s_cnt;
   const int64_t seg = blockIdx.x;
+  if (mask && mask[seg * mask_stride] >= 0) return;
   const uint64_t* src = in + seg * in_stride;
   uint64_t* dst = out + seg * out_stride;
   uint64_t prefix = 0;
@@ -124,11 +128,12 @@ __global__ void __launch_bounds__(NT) k2_select_compact(const uint64_t* __restri
 // one CTA per segment; the epilogue writes the sorted keys out.
 template <int DT, int NT, int ITEMS, bool DECODE>
 __global__ void __launch_bounds__(NT) k2_global_lsd(uint64_t* __restrict__ A, uint64_t* __restrict__ B,
-                                                    int64_t stride, int64_t kk,
+                                                    int64_t stride_a, int64_t stride_b, int64_t kk,
                                                     uint64_t* __restrict__ out_keys,
                                                     void* __restrict__ out_vals,
                                                     int64_t* __restrict__ out_idx,
-                                                    int64_t out_stride, CompGeo g) {
+                                                    int64_t out_stride, CompGeo g,
+                                                    const int* mask, int64_t mask_stride) {
   constexpr int N = NT * ITEMS;
   constexpr int NW = NT / 32;
   __shared__ uint32_t whist[NW * RADIX];
@@ -137,8 +142,9 @@ __global__ void __launch_bounds__(NT) k2_global_lsd(uint64_t* __restrict__ A, ui
   __shared__ uint32_t ghist[RADIX];
   __shared__ int s_skip;
   const int64_t seg = blockIdx.x;
-  uint64_t* src = A + seg * stride;
-  uint64_t* dst = B + seg * stride;
+  if (mask && mask[seg * mask_stride] >= 0) return;
+  uint64_t* src = A + seg * stride_a;
+  uint64_t* dst = B + seg * stride_b;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int shift = 1; shift < g.nbits; shift += 8) {
     for (int j = threadIdx.x; j < RADIX; j += NT) ghist[j] = 0;
@@ -214,7 +220,7 @@ static cudaError_t launch_small(const K2Args& a, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   if (a.nseg == 0) return cudaSuccess;
   kern<<<(unsigned)a.nseg, NT, sm, st>>>(a.in, a.in_stride, a.L, a.kk, a.out_keys, a.out_vals,
-                                         a.out_idx, a.out_stride, a.geo, lognb);
+                                         a.out_idx, a.out_stride, a.geo, lognb, a.mask, a.mask_stride);
   return cudaGetLastError();
 }
 
@@ -233,19 +239,23 @@ static cudaError_t run_k2_t(const K2Args& a, cudaStream_t st) {
   if (a.L <= K2_SMALL_CAP) return run_small<DT, DECODE>(a, st);
   // long segments
   if (a.scratch_a == nullptr || a.scratch_b == nullptr) return cudaErrorInvalidValue;
+  const int64_t sa = a.scratch_a_stride ? a.scratch_a_stride : a.kk;
+  const int64_t sb = a.scratch_b_stride ? a.scratch_b_stride : a.kk;
   k2_select_compact<1024><<<(unsigned)a.nseg, 1024, 0, st>>>(a.in, a.in_stride, a.L, a.kk,
-                                                             a.scratch_a, a.kk, a.geo.nbits);
+                                                             a.scratch_a, sa, a.geo.nbits, a.mask,
+                                                             a.mask_stride);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (a.kk <= K2_SMALL_CAP) {
     K2Args b = a;
     b.in = a.scratch_a;
-    b.in_stride = a.kk;
+    b.in_stride = sa;
     b.L = a.kk;
     return run_small<DT, DECODE>(b, st);
   }
   k2_global_lsd<DT, 512, 8, DECODE><<<(unsigned)a.nseg, 512, 0, st>>>(
-      a.scratch_a, a.scratch_b, a.kk, a.kk, a.out_keys, a.out_vals, a.out_idx, a.out_stride, a.geo);
+      a.scratch_a, a.scratch_b, sa, sb, a.kk, a.out_keys, a.out_vals, a.out_idx, a.out_stride, a.geo,
+      a.mask, a.mask_stride);
   return cudaGetLastError();
 }
 

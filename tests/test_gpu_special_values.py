@@ -92,7 +92,7 @@ def test_every_family_special_values(dn):
         1: (3, 65536, 64, 64, 1),          # narrow
         2: (2, 65536, 8192, 4096, 2),      # wide
         3: (1200, 2048, 64, 64, 1),        # rows (m >= 8 * #SMs)
-        4: (2, 131072, 16384, 16384, 2),   # s1_vec pool + select/compact + smem sort
+        7: (2, 131072, 16384, 16384, 2),   # s1_vec pool + histogram-chunked Stage 2
         0: (2, 20000, 700, 999, 3),        # generic (b % V != 0)
         5: (2, 30000, 300, 1, 300),        # materialise (b == 1)
     }
@@ -107,14 +107,22 @@ def test_every_family_special_values(dn):
         check(special(rng, kind, m, n, dn), dn, k, b, kb, btk.Assignment.CONTIGUOUS)
 
 
+@pytest.mark.parametrize("chunked", ["1", "0"])
 @pytest.mark.parametrize("dn", ["f32", "bf16", "f16"])
-def test_long_pool_global_sort_special_values(dn):
-    """Pool > 16384 and k > 16384: select/compact + the global LSD sort."""
+def test_long_pool_special_values(dn, chunked, monkeypatch):
+    """Pool > 16384: the histogram-chunked Stage 2 (its per-row radix-select
+    fallback for tie-heavy rows included), and with BTK_POOL_CHUNKED=0 the
+    select/compact + global LSD path."""
+    monkeypatch.setenv("BTK_POOL_CHUNKED", chunked)
     rng = np.random.default_rng(5)
-    m, n, k, b, kb = 2, 262144, 20000, 16384, 2
-    assert family(m, n, k, b, kb, dn) == 4
-    for kind in ("subnormal", "pm0"):
-        check(special(rng, kind, m, n, dn), dn, k, b, kb)
+    for (m, n, k, b, kb) in [(2, 262144, 20000, 16384, 2), (3, 131072, 12000, 16384, 2)]:
+        assert family(m, n, k, b, kb, dn) == (7 if chunked == "1" else 4)
+        for kind in ("subnormal", "pm0", "subnormal_ties"):
+            check(special(rng, kind, m, n, dn), dn, k, b, kb)
+        # mixed rows: tie-heavy rows take the fallback, normal rows the chunks
+        x32 = special(rng, "pm0", m, n, dn)
+        x32[1] = torch.from_numpy(rng.standard_normal(n, dtype=np.float32)).to(TORCH[dn]).float().numpy()
+        check(x32, dn, k, b, kb)
 
 
 @pytest.mark.parametrize("dn", ["f32", "bf16", "f16"])
