@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("BTK_LIB") or os.path.join(_HERE, "libbtk.so")
 
 BTK_F32, BTK_BF16, BTK_F16, BTK_F64 = 0, 1, 2, 3
 (BTK_FAM_GENERIC, BTK_FAM_NARROW, BTK_FAM_WIDE, BTK_FAM_ROWS, BTK_FAM_VEC_POOL, BTK_FAM_MATERIALIZE,
- BTK_FAM_F64, BTK_FAM_POOL_CHUNKED) = range(8)
+ BTK_FAM_F64, BTK_FAM_POOL_CHUNKED, BTK_FAM_XCHG) = range(9)
 BTK_INTERLEAVED, BTK_CONTIGUOUS = 0, 1
 
 _i64, _sz, _vp, _i = ctypes.c_int64, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_int

@@ -152,7 +152,8 @@ size_t btk_workspace_bytes(int64_t m, int64_t n, int64_t k, int64_t b, int64_t k
   p.m = m; p.n = n; p.k = k; p.b = b; p.kb = kb;
   p.layout = layout;
   p.geo = geo_for(dtype, n);
-  return std::max({plan_generic(m, n, k, b, kb).total(), plan_for(p).total(), fused_workspace_bytes(p)});
+  return std::max({plan_generic(m, n, k, b, kb).total(), plan_for(p).total(), fused_workspace_bytes(p),
+                   xchg_supported(p) ? xchg_workspace_bytes(p) : (size_t)0});
 }
 
 size_t btk_plan_workspace_bytes(const void* x, int64_t row_stride, int dtype, int64_t m, int64_t n,
@@ -166,6 +167,7 @@ size_t btk_plan_workspace_bytes(const void* x, int64_t row_stride, int dtype, in
   p.m = m; p.n = n; p.k = k; p.b = b; p.kb = kb;
   p.layout = layout;
   p.geo = geo_for(dtype, n);
+  if (xchg_supported(p)) return xchg_workspace_bytes(p);
   if (fused_supported(p)) return fused_workspace_bytes(p);
   return plan_for(p).total();
 }
@@ -180,7 +182,7 @@ int btk_uses_fused_path(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, 
   p.m = m; p.n = n; p.k = k; p.b = b; p.kb = kb;
   p.layout = layout;
   p.geo = geo_for(dtype, n);
-  return fused_supported(p) ? 1 : 0;
+  return (xchg_supported(p) || fused_supported(p)) ? 1 : 0;
 }
 
 int btk_kernel_family(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, int dtype,
@@ -194,6 +196,7 @@ int btk_kernel_family(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, in
   p.m = m; p.n = n; p.k = k; p.b = b; p.kb = kb;
   p.layout = layout;
   p.geo = geo_for(dtype, n);
+  if (xchg_supported(p)) return BTK_FAM_XCHG;
   const int fk = fused_kind(p);
   if (fk) return fk;  // BTK_FAM_NARROW / WIDE / ROWS
   if (b == 1 || kb > 16) return BTK_FAM_MATERIALIZE;
@@ -204,6 +207,14 @@ int btk_kernel_family(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, in
 int btk_launch_count(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, int dtype,
                      int layout, int64_t row_stride) {
   if (btk_validate(m, n, k, b, kb) != BTK_OK || !dtype_ok(dtype)) return 0;
+  if (dtype != BTK_F64) {
+    Problem p{};
+    p.x = reinterpret_cast<const void*>(uintptr_t(256));
+    p.row_stride = row_stride; p.dtype = dtype;
+    p.m = m; p.n = n; p.k = k; p.b = b; p.kb = kb; p.layout = layout; p.geo = geo_for(dtype, n);
+    // fused_xchg + the row-masked K2 of partition-overflow rows (1 or 2 kernels)
+    if (xchg_supported(p)) return 1 + (b * kb <= K2_SMALL_CAP ? 1 : 2);
+  }
   if (btk_uses_fused_path(m, n, k, b, kb, dtype, layout, row_stride)) return 1;
   if (dtype == BTK_F64) {
     auto segn = [](int64_t L, int64_t kk) { return L <= 8192 ? 1 : (kk <= 8192 ? 2 : 2); };
@@ -246,6 +257,11 @@ int btk_approx_topk(const void* x, int64_t row_stride, int dtype, int64_t m, int
   p.layout = layout;
   p.geo = geo_for(dtype, n);
   p.flag = flag;
+  if (xchg_supported(p)) {
+    const size_t need = xchg_workspace_bytes(p);
+    if (ws_bytes < need || (reinterpret_cast<uintptr_t>(ws) & 255)) return BTK_ERR_WORKSPACE;
+    return cuda_status(run_xchg(p, ws, out_vals, out_idx, st));
+  }
   if (fused_supported(p)) {
     const size_t need = fused_workspace_bytes(p);
     if (ws_bytes < need || (need && (reinterpret_cast<uintptr_t>(ws) & 255))) return BTK_ERR_WORKSPACE;

@@ -31,7 +31,8 @@ bool stage1_vec_supported(const Problem& p) {
 }
 
 template <int DT, int KB>
-static cudaError_t launch_s1_vec(const Problem& p, uint64_t* pool, uint32_t* hist, cudaStream_t st) {
+static cudaError_t launch_s1_vec(const Problem& p, uint64_t* pool, uint32_t* hist, cudaStream_t st,
+                                 const int* rowmask) {
   constexpr int V = Vec<DT>::V;
   const int64_t G = p.b / V, s = (p.n + p.b - 1) / p.b;
   const int last_vec = (int)((p.n - (s - 1) * p.b) / V);
@@ -41,32 +42,34 @@ static cudaError_t launch_s1_vec(const Problem& p, uint64_t* pool, uint32_t* his
   const int groups = (hist && p.m * ngrp >= 148 * 32) ? 4 : 1;
   dim3 grid((unsigned)((ngrp + groups - 1) / groups), (unsigned)p.m);
   if (hist) {
-    if (s <= 16) s1_vec<DT, KB, 16, true><<<grid, 256, 0, st>>>(p.x, p.row_stride, p.n, p.b, s, G, last_vec, p.geo, pool, p.flag, hist, groups);
-    else s1_vec<DT, KB, 8, true><<<grid, 256, 0, st>>>(p.x, p.row_stride, p.n, p.b, s, G, last_vec, p.geo, pool, p.flag, hist, groups);
+    if (s <= 16) s1_vec<DT, KB, 16, true><<<grid, 256, 0, st>>>(p.x, p.row_stride, p.n, p.b, s, G, last_vec, p.geo, pool, p.flag, hist, groups, rowmask);
+    else s1_vec<DT, KB, 8, true><<<grid, 256, 0, st>>>(p.x, p.row_stride, p.n, p.b, s, G, last_vec, p.geo, pool, p.flag, hist, groups, rowmask);
   } else {
-    if (s <= 16) s1_vec<DT, KB, 16, false><<<grid, 256, 0, st>>>(p.x, p.row_stride, p.n, p.b, s, G, last_vec, p.geo, pool, p.flag, nullptr, groups);
-    else s1_vec<DT, KB, 8, false><<<grid, 256, 0, st>>>(p.x, p.row_stride, p.n, p.b, s, G, last_vec, p.geo, pool, p.flag, nullptr, groups);
+    if (s <= 16) s1_vec<DT, KB, 16, false><<<grid, 256, 0, st>>>(p.x, p.row_stride, p.n, p.b, s, G, last_vec, p.geo, pool, p.flag, nullptr, groups, rowmask);
+    else s1_vec<DT, KB, 8, false><<<grid, 256, 0, st>>>(p.x, p.row_stride, p.n, p.b, s, G, last_vec, p.geo, pool, p.flag, nullptr, groups, rowmask);
   }
   return cudaGetLastError();
 }
 
 template <int DT>
-static cudaError_t s1_vec_dt(const Problem& p, uint64_t* pool, uint32_t* hist, cudaStream_t st) {
+static cudaError_t s1_vec_dt(const Problem& p, uint64_t* pool, uint32_t* hist, cudaStream_t st,
+                             const int* rowmask) {
   switch (p.kb) {
-    case 1: return launch_s1_vec<DT, 1>(p, pool, hist, st);
-    case 2: return launch_s1_vec<DT, 2>(p, pool, hist, st);
-    case 4: return launch_s1_vec<DT, 4>(p, pool, hist, st);
+    case 1: return launch_s1_vec<DT, 1>(p, pool, hist, st, rowmask);
+    case 2: return launch_s1_vec<DT, 2>(p, pool, hist, st, rowmask);
+    case 4: return launch_s1_vec<DT, 4>(p, pool, hist, st, rowmask);
   }
-  if constexpr (Vec<DT>::V * 8 <= 16) return launch_s1_vec<DT, 8>(p, pool, hist, st);
+  if constexpr (Vec<DT>::V * 8 <= 16) return launch_s1_vec<DT, 8>(p, pool, hist, st, rowmask);
   return cudaErrorNotSupported;
 }
 
-cudaError_t run_stage1_vec(const Problem& p, uint64_t* pool, cudaStream_t st, uint32_t* hist) {
+cudaError_t run_stage1_vec(const Problem& p, uint64_t* pool, cudaStream_t st, uint32_t* hist,
+                           const int* rowmask) {
   if (!stage1_vec_supported(p)) return cudaErrorNotSupported;
   switch (p.dtype) {
-    case F32: return s1_vec_dt<F32>(p, pool, hist, st);
-    case BF16: return s1_vec_dt<BF16>(p, pool, hist, st);
-    case F16: return s1_vec_dt<F16>(p, pool, hist, st);
+    case F32: return s1_vec_dt<F32>(p, pool, hist, st, rowmask);
+    case BF16: return s1_vec_dt<BF16>(p, pool, hist, st, rowmask);
+    case F16: return s1_vec_dt<F16>(p, pool, hist, st, rowmask);
   }
   return cudaErrorInvalidValue;
 }

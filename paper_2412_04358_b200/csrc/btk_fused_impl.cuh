@@ -473,6 +473,84 @@ struct Scanner16x2 {
 template <> struct Scanner<BF16, 1> : Scanner16x2<BF16> {};
 template <> struct Scanner<F16, 1> : Scanner16x2<F16> {};
 
+// k_b = 2 on 16-bit data, packed like Scanner16x2: per 32-bit word two
+// HSET2 masks (x > first, x > second) and bit-selects that shift the first
+// into second place when x beats it -> ~4 instructions per element.  Ties
+// keep the earlier slot (strict >), as the float Queue does.
+template <int DT>
+struct Scanner16x2K2 {
+  using S1 = Scanner16x2<DT>;
+  uint32_t m1[4], m2[4], c1[4], c2[4], nf2[4];
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      m1[w] = m2[w] = S1::NEG_INF2;
+      c1[w] = c2[w] = 0xFFFFFFFFu;
+      nf2[w] = 0u;
+    }
+  }
+  __device__ __forceinline__ void row(const uint4& v, int trel) {
+    const uint32_t code = (uint32_t)trel * 0x10001u;
+    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const uint32_t x = w4[w];
+      const uint32_t g1 = S1::gt_mask(x, m1[w]);
+      const uint32_t g2 = S1::gt_mask(x, m2[w]);
+      const uint32_t s2 = (x & g2) | (m2[w] & ~g2);
+      const uint32_t t2 = (code & g2) | (c2[w] & ~g2);
+      m2[w] = (m1[w] & g1) | (s2 & ~g1);
+      c2[w] = (c1[w] & g1) | (t2 & ~g1);
+      m1[w] = (x & g1) | (m1[w] & ~g1);
+      c1[w] = (code & g1) | (c1[w] & ~g1);
+      nf2[w] = S1::fma0(x, nf2[w]);
+    }
+  }
+  __device__ __forceinline__ bool nonfinite() const {
+    constexpr uint32_t E = DT == BF16 ? 0x7F80u : 0x7C00u;
+    bool bad = false;
+#pragma unroll
+    for (int w = 0; w < 4; ++w)
+      bad |= ((nf2[w] & 0x7FFFu) > E) || (((nf2[w] >> 16) & 0x7FFFu) > E);
+    return bad;
+  }
+  template <int KBS>
+  __device__ __forceinline__ void spill(uint64_t* dst, int g, int64_t b, int64_t t_begin,
+                                        const CompGeo& geo) const {
+    each_comp(g, b, t_begin, geo, [&](int64_t col, int z, uint64_t c) {
+      dst[col * KBS + z] = c;
+      if (z == 1) {
+#pragma unroll
+        for (int q = 2; q < KBS; ++q) dst[col * KBS + q] = 0ull;
+      }
+    });
+  }
+  template <class F>
+  __device__ __forceinline__ void each_comp(int g, int64_t b, int64_t t_begin, const CompGeo& geo,
+                                            F&& f) const {
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t col = (int64_t)g * 8 + 2 * w + h;
+#pragma unroll
+        for (int z = 0; z < 2; ++z) {
+          const uint32_t raw = ((z ? m2[w] : m1[w]) >> (16 * h)) & 0xFFFFu;
+          const uint32_t code = ((z ? c2[w] : c1[w]) >> (16 * h)) & 0xFFFFu;
+          uint64_t c = 0ull;
+          if (code != 0xFFFFu) {
+            const int64_t idx = (t_begin + code) * b + col;
+            c = make_comp(vkey<DT>(raw), (uint32_t)idx, is_negzero<DT>(raw), geo);
+          }
+          f(col, z, c);
+        }
+      }
+    }
+  }
+};
+template <> struct Scanner<BF16, 2> : Scanner16x2K2<BF16> {};
+template <> struct Scanner<F16, 2> : Scanner16x2K2<F16> {};
+
 // ============================================================ narrow (TMA ring, cluster)
 struct NarrowArgs {
   const void* x;
@@ -857,12 +935,14 @@ __global__ void __launch_bounds__(256) s1_vec(const void* __restrict__ x, int64_
                                               int64_t n, int64_t b, int64_t s, int64_t G,
                                               int last_vec, CompGeo geo,
                                               uint64_t* __restrict__ pool, uint32_t* flag,
-                                              uint32_t* __restrict__ hist, int groups) {
+                                              uint32_t* __restrict__ hist, int groups,
+                                              const int* __restrict__ rowmask) {
   constexpr int V = Vec<DT>::V;
   constexpr int ESZ = VT<DT>::W / 8;
   constexpr int NBINS = HIST ? (1 << POOL_HBITS) : 1;
   __shared__ uint32_t sh[NBINS];
   const int64_t row = blockIdx.y;
+  if (rowmask && rowmask[row] >= 0) return;  // row already handled (btk_xchg.cu fallback mask)
   const int hshift = geo.nbits - POOL_HBITS;
   uint32_t bad = 0;
   if constexpr (HIST) {

@@ -90,7 +90,13 @@ cudaError_t run_stage1_generic(const Problem& p, uint64_t* pool, cudaStream_t st
 // V*k_b <= 16, 16-byte aligned rows); cudaErrorNotSupported otherwise.
 bool stage1_vec_supported(const Problem& p);
 cudaError_t run_stage1_vec(const Problem& p, uint64_t* pool, cudaStream_t st,
-                           uint32_t* hist = nullptr);
+                           uint32_t* hist = nullptr, const int* rowmask = nullptr);
+// Cluster-exchange fused kernel for large pools (btk_xchg.cu): Stage 1 and
+// Stage 2 of a row in one cluster launch, plus the row-masked generic
+// fallback for rows whose value partition overflows.
+bool xchg_supported(const Problem& p);
+size_t xchg_workspace_bytes(const Problem& p);
+cudaError_t run_xchg(const Problem& p, void* ws, void* out_vals, int64_t* out_idx, cudaStream_t st);
 // Chunked Stage 2 over a stage-1 pool with its coarse histogram.
 bool pool_chunked_ok(const Problem& p);
 size_t pool_chunked_bytes(const Problem& p);  // hist + tab + chunk buffer

@@ -1,0 +1,723 @@
+// Cluster-exchange fused kernel ("xchg"): Stage 1 + Stage 2 of one row in
+// ONE launch for large pools (cfg5: 131072 survivors per row, k = 65536;
+// cfg2: 16384 survivors = k), with no HBM round trip for the candidates.
+//
+// Restates reference approx.py:208-282 (stage1 + topk_with_indices) and
+// exact.py:130-159 (_canonical_order) for the B200: a cluster of C CTAs
+// owns one row; the row's b buckets (interleaved: the columns of the row
+// viewed as (s, b), approx.py:112-131) are split into C column ranges.
+//
+//   1. stage 1    CTA r streams its b/C columns (16-byte LDGs, all s
+//                 view-rows of a vector column in flight) and keeps the top
+//                 k_b (value, slot) per column in registers (strict ">" on
+//                 ascending slots == first maximum, approx.py:151-162).  The
+//                 survivors go to a shared-memory candidate array in column
+//                 (= bucket id j) order.
+//   2. splitters  every CTA ranks a strided sample of its candidates and
+//                 stores its local quantiles (C-1 owner boundaries and a
+//                 conservative selection threshold: the sample rank of k
+//                 plus 4 sigma) into every CTA; after one barrier the CTAs
+//                 average them, so each owner range holds ~k/C keys.  Only
+//                 splitters come from the sample; every count below is
+//                 exact.
+//   3. exchange   each thread counts its (column-ordered) candidates per
+//                 owner; block and cluster prefix sums give every candidate
+//                 a stable slot in its owner's receive buffer, written with
+//                 st.shared::cluster.  Arrival order is source rank, then
+//                 column: every receive buffer is sorted by bucket id j.
+//                 The exact per-owner totals give each owner its output
+//                 offset; a row whose threshold kept < k keys or whose
+//                 owner overflowed takes the fallback below.
+//   4. sort       each owner sorts its keys descending with stable 4-bit
+//                 LSD passes (per-thread packed counters, block scan), only
+//                 over bits that vary, and never over the j bits: a key's
+//                 index field is (~t | ~j) for idx = t*b + j (b a power of
+//                 two) and the buffer already is in ascending-j order.
+//   5. emit       the owner decodes its first min(count, k - start) keys
+//                 into (value bits, int64 index) at its output offset.
+//
+// Fallback rows (rowmask = -1: partition overflow, or a 16-bit owner range
+// too wide for 32-bit sort keys) write their Stage-1 survivors in the
+// generic pool layout, and the row-masked K2 (btk_select.cu) launched
+// right after finishes them; other rows make it exit at once.
+//
+// Keys: for 16-bit dtypes a candidate is a 32-bit record
+// (vkey16 << 16 | (0x7FFF - t) << 1 | negzero) with j implied by its
+// position, and the sort key is (comp - base_r) in 32 bits, base_r the
+// owner's range floor aligned to the value field; fp32 uses the 64-bit
+// composite key (btk_common.cuh) throughout.
+#include "btk_fused_impl.cuh"
+
+namespace btk {
+namespace xc {
+using namespace fz;
+
+// --------------------------------------------------------------- DSMEM helpers
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ uint32_t ld_cl_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_cl_u64(uint32_t a) {
+  uint64_t v;
+  asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_cl(uint32_t a, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_cl(uint32_t a, uint64_t v) {
+  asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  cluster_arrive_release();
+  cluster_wait_acquire();
+}
+
+// padded record index: one record of padding per 128 bytes, so a thread's
+// consecutive records (blocked layouts) are bank-conflict free
+template <typename KT>
+__host__ __device__ constexpr int padk(int p) {
+  return sizeof(KT) == 4 ? p + (p >> 5) : p + (p >> 4);
+}
+
+constexpr int SPC = 128;  // sample keys per CTA
+
+struct XArgs {
+  const void* x;
+  int64_t row_stride;
+  int64_t m, n, k, b;
+  int s, logb, cols, ncand;
+  CompGeo geo;
+  void* out_vals;
+  int64_t* out_idx;
+  uint32_t* flag;
+  int* rowmask;    // per row: 0 handled here, -1 generic fallback
+  uint64_t* pool;  // fallback rows: m x (b*k_b) comps, bucket-major (s1_vec layout)
+  int trace;       // development timeline (BTK_XC_TRACE=1): globaltimer per CTA and phase
+};
+
+constexpr int TRACE_CTAS = 16384;
+static __device__ unsigned long long g_xtrace[TRACE_CTAS][8];
+__device__ __forceinline__ void mark(const XArgs& a, int ph) {
+  if (a.trace && threadIdx.x == 0 && blockIdx.x < TRACE_CTAS) g_xtrace[blockIdx.x][ph] = gtime();
+}
+
+// candidate record <-> composite key
+template <typename KT>
+__device__ __forceinline__ KT to_rec(uint64_t c, const XArgs& a) {
+  if constexpr (sizeof(KT) == 8) {
+    return c;
+  } else {
+    const uint32_t vk = (uint32_t)(c >> (a.geo.ib + 1));
+    const uint32_t idx = a.geo.imax - (uint32_t)((c >> 1) & a.geo.imax);
+    const uint32_t t = idx >> a.logb;
+    return (vk << 16) | ((0x7FFFu - t) << 1) | (uint32_t)(c & 1u);
+  }
+}
+template <typename KT>
+__device__ __forceinline__ uint64_t from_rec(KT r, uint32_t j, const XArgs& a) {
+  if constexpr (sizeof(KT) == 8) {
+    return r;
+  } else {
+    const uint32_t t = 0x7FFFu - ((r >> 1) & 0x7FFFu);
+    return make_comp(r >> 16, (t << a.logb) | j, r & 1u, a.geo);
+  }
+}
+
+// Block-wide digit scan over per-thread counters kept in shared memory:
+// cnt[q * NT + tid] packs the thread's counts of digits 2q (low 16 bits)
+// and 2q+1 (high 16 bits), q < 8.  On return cnt holds the thread's
+// exclusive base per digit (within the digit, in thread order), tot[d] the
+// block total of digit d and dex[d] the digit-concatenated exclusive base.
+template <int NT>
+__device__ __forceinline__ void digit_scan(uint32_t* cnt, uint32_t (*ws)[8], uint32_t* tot, uint32_t* dex) {
+  constexpr int NW = NT / 32;
+  constexpr int GW = NW / 4;  // warps per group in the cross-warp scan
+  static_assert(NW % 4 == 0, "NT multiple of 128");
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t own[8], w[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) w[q] = own[q] = cnt[q * NT + tid];
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, w[q], o);
+      if (lane >= o) w[q] += t;
+    }
+  }
+  if (lane == 31) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) ws[warp][q] = w[q];
+  }
+  __syncthreads();
+  if (warp == 0) {  // lane = word q (lane & 7) x warp group g (lane >> 3)
+    const int q = lane & 7, g = lane >> 3;
+    uint32_t v[GW], s4 = 0;
+#pragma unroll
+    for (int i = 0; i < GW; ++i) { v[i] = ws[g * GW + i][q]; s4 += v[i]; }
+    uint32_t x = s4;
+    uint32_t t = __shfl_up_sync(0xFFFFFFFFu, x, 8);
+    if (g >= 1) x += t;
+    t = __shfl_up_sync(0xFFFFFFFFu, x, 16);
+    if (g >= 2) x += t;
+    uint32_t run = x - s4;
+#pragma unroll
+    for (int i = 0; i < GW; ++i) { ws[g * GW + i][q] = run; run += v[i]; }
+    const uint32_t all = __shfl_sync(0xFFFFFFFFu, x, 24 + q);  // word q total (group 3 inclusive)
+    if (g == 0) {
+      const uint32_t lo = all & 0xFFFFu, hi = all >> 16, pair = lo + hi;
+      uint32_t e = pair;
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0x000000FFu, e, o);
+        if (q >= o) e += u;
+      }
+      e -= pair;
+      tot[2 * q] = lo;
+      tot[2 * q + 1] = hi;
+      dex[2 * q] = e;
+      dex[2 * q + 1] = e + lo;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 8; ++q) cnt[q * NT + tid] = w[q] - own[q] + ws[warp][q];
+}
+
+// count one item of digit d (< 16) in the thread's smem counters; returns
+// the number of earlier items of this thread with that digit
+template <int NT>
+__device__ __forceinline__ uint32_t count_digit(uint32_t* cnt, uint32_t d) {
+  uint32_t* c = cnt + (d >> 1) * NT + threadIdx.x;
+  const uint32_t sh = (d & 1u) << 4;
+  const uint32_t v = *c;
+  *c = v + (1u << sh);
+  return (v >> sh) & 0xFFFFu;
+}
+template <int NT>
+__device__ __forceinline__ uint32_t digit_base(const uint32_t* cnt, uint32_t d) {
+  return (cnt[(d >> 1) * NT + threadIdx.x] >> ((d & 1u) << 4)) & 0xFFFFu;
+}
+
+// Shared-memory carve-up (bytes), identical on host and device.
+constexpr int LUTN = 8192;  // 16-bit owner table: vkeys above the threshold
+template <typename KT, int NT, int IPT, int ITEMS>
+struct Layout {
+  static constexpr int CAP = NT * ITEMS;
+  static constexpr size_t CAND = ((size_t)padk<KT>(NT * IPT) * sizeof(KT) + 127) / 128 * 128;
+  static constexpr size_t BUF = ((size_t)padk<KT>(CAP) * sizeof(KT) + 127) / 128 * 128;
+  static constexpr size_t A = 0;                 // candidates, later the sort's partner buffer
+  static constexpr size_t B = A + (CAND > BUF ? CAND : BUF);  // receive buffer (the sample first)
+  static constexpr size_t CNT = B + BUF;         // u32 [8][NT] digit counters / bases
+  static constexpr size_t LUT = CNT + (size_t)NT * 8 * 4;  // u8 owner per vkey (16-bit dtypes)
+  static constexpr size_t BYTES = LUT + (sizeof(KT) == 4 ? LUTN : 0);
+};
+
+template <int DT, int KB, int C, int NT, int IPT, int ITEMS, typename KT>
+__global__ void __launch_bounds__(NT, 2) fused_xchg(XArgs a) {
+  constexpr int V = Vec<DT>::V;
+  constexpr int ESZ = VT<DT>::W / 8;
+  constexpr int NW = NT / 32;
+  constexpr int CAP = NT * ITEMS;
+  constexpr int U = 8;  // 16-byte loads in flight per thread
+  constexpr bool K32 = sizeof(KT) == 4;
+  using L = Layout<KT, NT, IPT, ITEMS>;
+  static_assert(C <= 16 && (C & (C - 1)) == 0, "cluster");
+  static_assert(2 * SPC * 8 <= L::BUF, "sample fits the receive buffer");
+  extern __shared__ __align__(128) uint8_t smem[];
+  KT* cand = reinterpret_cast<KT*>(smem + L::A);
+  KT* recv = reinterpret_cast<KT*>(smem + L::B);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + L::CNT);
+  uint8_t* lut = smem + L::LUT;
+  __shared__ uint32_t ws[NW][8];
+  __shared__ uint32_t dtot[16], dex[16];
+  __shared__ unsigned long long est[C][C + 1];   // every CTA's splitter estimates
+  __shared__ unsigned long long lspl[C + 1];     // the splitters (identical in every CTA);
+                                                 // 16-bit dtypes: vkeys, else comps
+  __shared__ unsigned long long s_max, s_min;
+  __shared__ uint32_t sendcnt[16], tot[C], dbase[C];
+  __shared__ unsigned long long s_vary, s_start;
+  __shared__ int s_why;
+
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint32_t rank = cta_rank();
+  const int64_t row = blockIdx.x / C;
+  const CompGeo geo = a.geo;
+  const int64_t col0 = (int64_t)rank * a.cols;
+  const int gv = a.cols / V;
+  const int ib1 = geo.ib + 1;
+
+  if (tid == 0) { s_max = 0ull; s_min = ~0ull; s_vary = 0ull; }
+  if (tid < C) { tot[tid] = 0u; dbase[tid] = 0u; }
+  __syncthreads();
+  pdl_trigger();
+  pdl_wait();
+  mark(a, 0);
+
+  // ---------------------------------------------------------------- 1. stage 1
+  {
+    uint32_t bad = 0;
+    uint64_t mx = 0ull, mn = ~0ull;
+    const uint8_t* rowp = static_cast<const uint8_t*>(a.x) + (row * a.row_stride + col0) * ESZ;
+    const int64_t vstride = a.b * ESZ;
+    for (int g = tid; g < gv; g += NT) {
+      Scanner<DT, KB> sc;
+      sc.init();
+      const uint8_t* colp = rowp + (int64_t)g * V * ESZ;
+      for (int t0 = 0; t0 < a.s; t0 += U) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          v[u] = (t0 + u < a.s) ? ldg_stream(colp + (int64_t)(t0 + u) * vstride) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (t0 + u < a.s) sc.row(v[u], t0 + u);
+      }
+      bad |= sc.nonfinite() ? 1u : 0u;
+      sc.each_comp((int)(col0 / V) + g, a.b, 0, geo, [&](int64_t col, int z, uint64_t c) {
+        cand[padk<KT>((int)((col - col0) * KB + z))] = to_rec<KT>(c, a);
+        mx = c > mx ? c : mx;
+        mn = c < mn ? c : mn;
+      });
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const uint64_t x1 = __shfl_xor_sync(0xFFFFFFFFu, mx, o), x2 = __shfl_xor_sync(0xFFFFFFFFu, mn, o);
+      mx = x1 > mx ? x1 : mx;
+      mn = x2 < mn ? x2 : mn;
+    }
+    if (lane == 0) {
+      atomicMax(&s_max, (unsigned long long)mx);
+      atomicMin(&s_min, (unsigned long long)mn);
+    }
+    if (__syncthreads_or(bad) && tid == 0 && a.flag) atomicOr(a.flag, 1u);
+  }
+  mark(a, 1);
+
+  // ---------------------------------------------------------------- 2. splitters
+  // Every CTA ranks a strided sample of SPC of its candidates (count of
+  // larger samples; comps are unique), takes its local quantiles at the
+  // owner boundaries and at the threshold rank, and stores them into every
+  // CTA; after one barrier each CTA averages the C estimates per splitter
+  // (identical data -> identical splitters in every CTA).  The averages
+  // are ordered because every CTA's quantiles are.  For 16-bit dtypes the
+  // splitters are then rounded down to whole values (vkeys), so a key's
+  // owner is a table lookup on its vkey.
+  int rthr = SPC;  // local sample rank of the threshold (k plus 4 sigma of the pooled sample)
+  {
+    const double q = (double)a.k / ((double)a.b * KB);
+    if (q < 1.0) {
+      const double r = SPC * q + 4.0 * sqrt(SPC * q * (1.0 - q) / C) + 0.5;
+      rthr = r >= (double)SPC ? SPC : (int)ceil(r);
+    }
+  }
+  const bool select_all = rthr >= SPC;
+  {
+    uint64_t* smp = reinterpret_cast<uint64_t*>(smem + L::B);  // SPC sampled comps
+    uint64_t* srt = smp + SPC;                                   // ranked
+    if (tid < SPC) {
+      const int stride = a.ncand / SPC;
+      // the in-stride offset varies with tid (odd step) so the sample covers
+      // every queue slot z = p % k_b, not one aliased slot
+      const int p = tid * stride + (int)(((uint64_t)row * 40503u + rank * 977u + tid * 7u) % (uint64_t)stride);
+      smp[tid] = from_rec<KT>(cand[padk<KT>(p)], (uint32_t)(col0 + p / KB), a);
+    }
+    __syncthreads();
+    if (tid < SPC) {
+      const uint64_t x = smp[tid];
+      int r = 0;
+#pragma unroll 8
+      for (int q = 0; q < SPC; ++q) r += smp[q] > x ? 1 : 0;
+      srt[r] = x;
+    }
+    __syncthreads();
+    if (tid <= C) {  // local estimate of splitter tid, stored into every CTA
+      uint64_t v;
+      if (tid == 0) v = s_max;
+      else if (tid < C) v = srt[(tid * rthr) / C];
+      else v = select_all ? s_min : srt[rthr];
+      const uint32_t dst = smem_u32(&est[rank][tid]);
+#pragma unroll 4
+      for (int r = 0; r < C; ++r) st_cl(mapa(dst, (uint32_t)r), v);
+    }
+  }
+  cluster_sync_all();  // A: every CTA's estimates everywhere
+  mark(a, 2);
+  if (tid <= C) {
+    uint64_t v;
+    if (tid == 0) {  // the cluster's max + 1 (exact)
+      v = est[0][0];
+      for (int r = 1; r < C; ++r) v = est[r][0] > v ? est[r][0] : v;
+      v = K32 ? (v >> ib1) + 1ull : v + 1ull;
+    } else if (tid == C && select_all) {  // the cluster's min (exact): everything is selected
+      v = est[0][C];
+      for (int r = 1; r < C; ++r) v = est[r][C] < v ? est[r][C] : v;
+      if (K32) v >>= ib1;
+    } else {
+      uint64_t sum = 0;
+      for (int r = 0; r < C; ++r) sum += est[r][tid];
+      v = sum / C;
+      if (K32) v >>= ib1;
+    }
+    lspl[tid] = v;
+  }
+  __syncthreads();
+  // 16-bit dtypes: owner table over the selected vkeys [lspl[C], lspl[0])
+  const uint32_t vthr = (uint32_t)lspl[C];
+  const uint32_t vspan = K32 ? (uint32_t)(lspl[0] - lspl[C]) : 0u;
+  const uint32_t vlim = vspan <= (uint32_t)LUTN ? vspan : 0u;  // too wide: fallback row
+  if constexpr (K32) {
+    if (vspan <= (uint32_t)LUTN) {
+      for (uint32_t i = tid; i < vspan; i += NT) {
+        const uint64_t v = vthr + i;
+        uint32_t o = 0;
+#pragma unroll
+        for (int c = 1; c < C; ++c) o += lspl[c] > v ? 1u : 0u;
+        lut[i] = (uint8_t)o;
+      }
+    }
+    __syncthreads();
+  }
+  mark(a, 3);
+
+  // ---------------------------------------------------------------- 3. exchange
+  // owner of a candidate: #{c in 1..C : spl[c] > key}; C = below the threshold
+  auto owner = [&](KT rec, uint32_t j) -> uint32_t {
+    if constexpr (K32) {
+      const uint32_t off = (rec >> 16) - vthr;  // wraps for vkeys below the threshold
+      return off < vlim ? (uint32_t)lut[off] : (uint32_t)C;
+    } else {
+      const uint64_t x = rec;
+      uint32_t o = 0;  // largest o with spl[o] > x (spl[0] exceeds every key)
+#pragma unroll
+      for (int st = C / 2; st > 0; st >>= 1)
+        if (x < lspl[o + st]) o += st;
+      if (x < lspl[C]) o = C;
+      return o;
+    }
+  };
+  // 32-bit sort key of a candidate for owner d: value offset above the
+  // owner's lowest vkey, then the complemented index, then negzero
+  auto key32 = [&](KT rec, uint32_t j, uint32_t d) -> uint32_t {
+    const uint32_t t = 0x7FFFu - ((rec >> 1) & 0x7FFFu);
+    const uint32_t idx = (t << a.logb) | j;
+    return (((uint32_t)(rec >> 16) - (uint32_t)lspl[d + 1]) << ib1) | ((geo.imax - idx) << 1) | (uint32_t)(rec & 1u);
+  };
+  const int p0 = tid * IPT;
+  uint32_t dl[IPT];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) cnt[q * NT + tid] = 0u;
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int p = p0 + i;
+    uint32_t d = (uint32_t)C;
+    if (p < a.ncand) d = owner(cand[padk<KT>(p)], (uint32_t)(col0 + p / KB));
+    dl[i] = d << 16;
+    if (d < (uint32_t)C) dl[i] |= count_digit<NT>(cnt, d);
+  }
+  digit_scan<NT>(cnt, ws, sendcnt, dex);
+  cluster_sync_all();  // C: send counts of every CTA published
+  mark(a, 4);
+  if (tid < C * C) {  // totals per owner and this CTA's base in each owner
+    const int r = tid / C, d = tid % C;
+    const uint32_t v = ld_cl_u32(mapa(smem_u32(&sendcnt[d]), (uint32_t)r));
+    if (v) {
+      atomicAdd(&tot[d], v);
+      if ((uint32_t)r < rank) atomicAdd(&dbase[d], v);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {  // fallback verdict, output offset and receive count (one thread)
+    uint64_t sum = 0, st = 0;
+    int why = 0;  // fallback reasons (rowmask = -1 - why): 1 overflow, 2 key range, 4 short
+    for (int d = 0; d < C; ++d) {
+      if ((uint32_t)d < rank) st += tot[d];
+      sum += tot[d];
+      if (tot[d] > (uint32_t)CAP) why |= 1;
+      // the owner's value offsets must fit the 32-bit key above the index field
+      if (K32 && tot[d] && ((lspl[d] - 1ull - lspl[d + 1]) >> (32 - ib1)) != 0ull) why |= 2;
+    }
+    if (K32 && vspan > (uint32_t)LUTN) why |= 2;
+    if (sum < (uint64_t)a.k) why |= 4;
+    s_start = st;
+    s_why = why;
+  }
+  __syncthreads();
+  const int64_t start = (int64_t)s_start;
+  const int R = (int)tot[rank];
+  if (s_why) {  // identical verdict in every CTA (same splitters, same totals)
+    if (rank == 0 && tid == 0) a.rowmask[row] = -1 - s_why;
+    uint64_t* dst = a.pool + row * a.b * KB + col0 * KB;
+    for (int p = tid; p < a.ncand; p += NT)
+      dst[p] = from_rec<KT>(cand[padk<KT>(p)], (uint32_t)(col0 + p / KB), a);
+    cluster_sync_all();  // peers may still read this CTA's send counts
+    return;
+  }
+  if (rank == 0 && tid == 0) a.rowmask[row] = 0;
+  {
+    const uint32_t recv_s = smem_u32(recv);
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const uint32_t d = dl[i] >> 16;
+      if (d < (uint32_t)C) {
+        const int p = p0 + i;
+        const KT rec = cand[padk<KT>(p)];
+        const uint32_t j = (uint32_t)(col0 + p / KB);
+        const uint32_t pos = dbase[d] + digit_base<NT>(cnt, d) + (dl[i] & 0xFFFFu);
+        const uint32_t dst = mapa(recv_s + (uint32_t)padk<KT>((int)pos) * (uint32_t)sizeof(KT), d);
+        if constexpr (K32) st_cl(dst, key32(rec, j, d));
+        else st_cl(dst, (uint64_t)rec);
+      }
+    }
+  }
+  cluster_sync_all();  // D: every receive buffer complete; no remote traffic after this
+  mark(a, 5);
+
+  // ---------------------------------------------------------------- 4. sort
+  const int items = (R + NT - 1) / NT;
+  {
+    KT vary = 0;
+    const KT k0 = R ? recv[0] : (KT)0;
+    for (int p = tid; p < items * NT; p += NT) {
+      if (p < R) vary |= recv[padk<KT>(p)] ^ k0;
+      else recv[padk<KT>(p)] = (KT)0;  // pads sort last
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) vary |= __shfl_xor_sync(0xFFFFFFFFu, vary, o);
+    if (lane == 0 && vary) atomicOr(&s_vary, (unsigned long long)vary);
+  }
+  __syncthreads();
+  KT* src = recv;
+  KT* dst = cand;
+  {
+    constexpr int KBITS = (int)sizeof(KT) * 8;
+    const KT vary = (KT)s_vary;
+    const int lowbit = 1 + a.logb;  // negzero and j bits: already in order
+    for (int shift = lowbit; shift < KBITS && (vary >> shift) != 0; shift += 4) {
+      if (((vary >> shift) & (KT)0xF) == 0) continue;
+      uint32_t sl[ITEMS];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) cnt[q * NT + tid] = 0u;
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        if (i < items) {
+          const KT key = src[padk<KT>(tid * items + i)];
+          const uint32_t d = 15u - (uint32_t)((key >> shift) & (KT)0xF);
+          sl[i] = (d << 16) | count_digit<NT>(cnt, d);
+        }
+      }
+      digit_scan<NT>(cnt, ws, dtot, dex);
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        if (i < items) {
+          const uint32_t d = sl[i] >> 16;
+          const int r = (int)(dex[d] + digit_base<NT>(cnt, d) + (sl[i] & 0xFFFFu));
+          dst[padk<KT>(r)] = src[padk<KT>(tid * items + i)];
+        }
+      }
+      __syncthreads();
+      KT* t = src; src = dst; dst = t;
+    }
+  }
+
+  // ---------------------------------------------------------------- 5. emit
+  mark(a, 6);
+  const int keep = (int)min((int64_t)R, a.k - start);
+  for (int q = tid; q < keep; q += NT) {
+    const KT key = src[padk<KT>(q)];
+    uint64_t c;
+    if constexpr (K32) {
+      c = ((uint64_t)((uint32_t)lspl[rank + 1] + (key >> ib1)) << ib1) | (uint64_t)(key & ((1u << ib1) - 1u));
+    } else {
+      c = key;
+    }
+    emit_comp<DT>(c, row * a.k + start + q, geo, a.out_vals, a.out_idx);
+  }
+  mark(a, 7);
+}
+
+// ================================================================ host side
+template <int DT> struct Cfg;
+template <> struct Cfg<F32> {
+  using KT = uint64_t;
+  static constexpr int C = 8, NT = 512, IPT = 8, ITEMS = 8;
+};
+template <> struct Cfg<BF16> {
+  using KT = uint32_t;
+  static constexpr int C = 16, NT = 512, IPT = 16, ITEMS = 16;
+};
+template <> struct Cfg<F16> : Cfg<BF16> {};
+
+inline bool pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+
+template <int DT>
+bool plan_t(const Problem& p, XArgs& a) {
+  using CF = Cfg<DT>;
+  constexpr int V = Vec<DT>::V;
+  const int esz = VT<DT>::W / 8;
+  if (p.layout != 0 || !(p.kb == 1 || p.kb == 2 || p.kb == 4 || (p.kb == 8 && DT == F32))) return false;
+  if (V * p.kb > 32) return false;
+  if (!pow2(p.b) || p.n % p.b) return false;
+  const int64_t s = p.n / p.b;
+  if (s < p.kb || s > 1024) return false;
+  if ((reinterpret_cast<uintptr_t>(p.x) & 15) || ((p.row_stride * esz) & 15)) return false;
+  if (p.b % ((int64_t)CF::C * V * 32)) return false;  // whole warps of vector columns per CTA
+  const int64_t cols = p.b / CF::C;
+  const int64_t ncand = cols * p.kb;
+  if (ncand > (int64_t)CF::IPT * CF::NT || ncand < SPC) return false;
+  // expected keys per owner (k/C plus the threshold margin) within ~half the receive capacity
+  if ((p.k + CF::C - 1) / CF::C > (int64_t)CF::NT * CF::ITEMS / 2) return false;
+  if (p.m * CF::C > 0x7FFFFFFFll) return false;
+  if (DT != F32 && p.geo.ib > 26) return false;
+  a.x = p.x; a.row_stride = p.row_stride;
+  a.m = p.m; a.n = p.n; a.k = p.k; a.b = p.b;
+  a.s = (int)s;
+  a.logb = 0;
+  while ((int64_t(1) << a.logb) < p.b) ++a.logb;
+  a.cols = (int)cols;
+  a.ncand = (int)ncand;
+  a.geo = p.geo;
+  a.flag = p.flag;
+  return true;
+}
+
+template <int DT, int KB>
+cudaError_t launch_t(const XArgs& a, cudaStream_t st) {
+  using CF = Cfg<DT>;
+  using KT = typename CF::KT;
+  using L = Layout<KT, CF::NT, CF::IPT, CF::ITEMS>;
+  auto kern = fused_xchg<DT, KB, CF::C, CF::NT, CF::IPT, CF::ITEMS, KT>;
+  static thread_local int attr_done = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_done != dev) {
+    cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)L::BYTES);
+    if (e != cudaSuccess) return e;
+    if (CF::C > 8) {
+      e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
+    attr_done = dev;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(a.m * CF::C));
+  cfg.blockDim = dim3(CF::NT);
+  cfg.dynamicSmemBytes = L::BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  attr[na].id = cudaLaunchAttributeClusterDimension;
+  attr[na].val.clusterDim.x = CF::C;
+  attr[na].val.clusterDim.y = 1;
+  attr[na].val.clusterDim.z = 1;
+  ++na;
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+template <int DT>
+cudaError_t launch_dt(const XArgs& a, int64_t kb, cudaStream_t st) {
+  switch (kb) {
+    case 1: return launch_t<DT, 1>(a, st);
+    case 2: return launch_t<DT, 2>(a, st);
+    case 4: return launch_t<DT, 4>(a, st);
+  }
+  if constexpr (DT == F32) return launch_t<DT, 8>(a, st);
+  return cudaErrorNotSupported;
+}
+
+bool plan(const Problem& p, XArgs& a) {
+  switch (p.dtype) {
+    case F32: return plan_t<F32>(p, a);
+    case BF16: return plan_t<BF16>(p, a);
+    case F16: return plan_t<F16>(p, a);
+  }
+  return false;
+}
+
+}  // namespace xc
+
+bool xchg_supported(const Problem& p) {
+  const int want = fz::env_int("BTK_XC", -1);
+  if (want == 0) return false;
+  // 16-bit dtypes with pools beyond one CTA's shared memory (<= 16384: the
+  // single-CTA fused kernels are faster; fp32: the chunked pool path, whose
+  // 64-bit keys this kernel sorts slower — BTK_XC=1 forces it for A/B runs)
+  if (want != 1 && (p.dtype == F32 || p.b * p.kb <= fz::FUSED_POOL_CAP)) return false;
+  if (p.b * p.kb < 8192) return false;
+  xc::XArgs a{};
+  return xc::plan(p, a);
+}
+
+static size_t al256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+size_t xchg_workspace_bytes(const Problem& p) {
+  // row mask + the generic fallback's pool (+ its long-segment scratch)
+  const int64_t P = p.b * p.kb;
+  size_t v = al256((size_t)p.m * 4) + al256((size_t)p.m * P * 8);
+  if (P > K2_SMALL_CAP) v += al256((size_t)p.m * p.k * 8);
+  return v;
+}
+
+cudaError_t run_xchg(const Problem& p, void* ws, void* out_vals, int64_t* out_idx, cudaStream_t st) {
+  xc::XArgs a{};
+  if (!xc::plan(p, a)) return cudaErrorNotSupported;
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  int* rowmask = reinterpret_cast<int*>(w);
+  w += al256((size_t)p.m * 4);
+  uint64_t* pool = reinterpret_cast<uint64_t*>(w);
+  const int64_t P = p.b * p.kb;
+  w += al256((size_t)p.m * P * 8);
+  uint64_t* scratch = P > K2_SMALL_CAP ? reinterpret_cast<uint64_t*>(w) : nullptr;
+  a.out_vals = out_vals;
+  a.out_idx = out_idx;
+  a.rowmask = rowmask;
+  a.pool = pool;
+  a.trace = fz::env_int("BTK_XC_TRACE", 0);
+  cudaError_t e = cudaErrorInvalidValue;
+  switch (p.dtype) {
+    case F32: e = xc::launch_dt<F32>(a, p.kb, st); break;
+    case BF16: e = xc::launch_dt<BF16>(a, p.kb, st); break;
+    case F16: e = xc::launch_dt<F16>(a, p.kb, st); break;
+  }
+  if (e != cudaSuccess) return e;
+  // rows the partition could not place (rowmask -1): K2 over their pools
+  K2Args k2{};
+  k2.in = pool; k2.in_stride = P; k2.nseg = p.m; k2.L = P; k2.kk = p.k;
+  k2.out_vals = out_vals; k2.out_idx = out_idx; k2.out_stride = p.k;
+  k2.geo = p.geo;
+  k2.scratch_a = scratch; k2.scratch_b = pool;
+  k2.scratch_a_stride = p.k; k2.scratch_b_stride = P;
+  k2.mask = rowmask;
+  k2.mask_stride = 1;
+  return run_k2(p.dtype, true, k2, st);
+}
+
+}  // namespace btk
+
+// Development timeline of the last traced fused_xchg launch (BTK_XC_TRACE=1):
+// per CTA, globaltimer at start, stage 1 done, after barriers A, B (+ splitter
+// copy), C, D, sort done, end.  Not part of the ABI.
+extern "C" int btk_xc_trace_read(void* host_dst, int nblocks) {
+  if (nblocks > btk::xc::TRACE_CTAS) nblocks = btk::xc::TRACE_CTAS;
+  return (int)cudaMemcpyFromSymbol(host_dst, btk::xc::g_xtrace, (size_t)nblocks * 8 * 8);
+}

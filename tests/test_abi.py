@@ -66,15 +66,15 @@ _PLANS = [
     (128, 65536, 16384, 2048, 8, _lib.BTK_F32, 1, 1),
     (128, 1 << 20, 256, 512, 1, _lib.BTK_BF16, 1, 1),       # cfg3
     (4096, 32768, 512, 512, 1, _lib.BTK_BF16, 1, 1),        # cfg4: warp-per-row kernel
-    (8192, 1 << 20, 65536, 65536, 2, _lib.BTK_BF16, 0, 5),  # cfg5: s1_vec+hist, scatter, chunk sort, masked fallback x2
+    (8192, 1 << 20, 65536, 65536, 2, _lib.BTK_BF16, 1, 3),  # cfg5: cluster exchange + masked fallback K2 x2
 ]
 
 
 @pytest.mark.parametrize("plan", _PLANS, ids=lambda p: f"m{p[0]}-n{p[1]}-k{p[2]}-b{p[3]}-kb{p[4]}")
 def test_launch_planner_host_side(plan):
     """The host-side planner (no GPU needed) picks the fused single-launch
-    path for cfg1-4 and the generic multi-kernel path for cfg5, and sizes
-    the workspace for the generic path."""
+    path for cfg1-4 and the cluster-exchange kernel (plus its row-masked
+    fallback K2) for cfg5, and sizes the workspace for the path that runs."""
     m, n, k, b, kb, dt, fused, launches = plan
     lib = _lib.load()
     assert lib.btk_uses_fused_path(m, n, k, b, kb, dt, _lib.BTK_INTERLEAVED, n) == fused

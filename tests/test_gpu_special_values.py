@@ -92,11 +92,14 @@ def test_every_family_special_values(dn):
         1: (3, 65536, 64, 64, 1),          # narrow
         2: (2, 65536, 8192, 4096, 2),      # wide
         3: (1200, 2048, 64, 64, 1),        # rows (m >= 8 * #SMs)
-        7: (2, 131072, 16384, 16384, 2),   # s1_vec pool + histogram-chunked Stage 2
+        7: (2, 131072, 16384, 16384, 2),   # s1_vec pool + histogram-chunked Stage 2 (fp32)
+        8: (2, 131072, 16384, 16384, 2),   # cluster exchange (16-bit; same shape)
         0: (2, 20000, 700, 999, 3),        # generic (b % V != 0)
         5: (2, 30000, 300, 1, 300),        # materialise (b == 1)
     }
     for fam, (m, n, k, b, kb) in cases.items():
+        if (fam == 7) != (dn == "f32") and fam in (7, 8):
+            continue  # large pools: fp32 -> chunked pool, 16-bit -> cluster exchange
         assert family(m, n, k, b, kb, dn) == fam, (fam, dn)
         for kind in KINDS:
             check(special(rng, kind, m, n, dn), dn, k, b, kb)
@@ -110,10 +113,12 @@ def test_every_family_special_values(dn):
 @pytest.mark.parametrize("chunked", ["1", "0"])
 @pytest.mark.parametrize("dn", ["f32", "bf16", "f16"])
 def test_long_pool_special_values(dn, chunked, monkeypatch):
-    """Pool > 16384: the histogram-chunked Stage 2 (its per-row radix-select
-    fallback for tie-heavy rows included), and with BTK_POOL_CHUNKED=0 the
+    """Pool > 16384 without the cluster exchange (BTK_XC=0): the
+    histogram-chunked Stage 2 (its per-row radix-select fallback for
+    tie-heavy rows included), and with BTK_POOL_CHUNKED=0 the
     select/compact + global LSD path."""
     monkeypatch.setenv("BTK_POOL_CHUNKED", chunked)
+    monkeypatch.setenv("BTK_XC", "0")
     rng = np.random.default_rng(5)
     for (m, n, k, b, kb) in [(2, 262144, 20000, 16384, 2), (3, 131072, 12000, 16384, 2)]:
         assert family(m, n, k, b, kb, dn) == (7 if chunked == "1" else 4)

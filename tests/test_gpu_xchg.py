@@ -1,0 +1,123 @@
+"""The cluster-exchange kernel (btk_xchg.cu, family BTK_FAM_XCHG) against
+the oracle: every 16-bit dtype and k_b it serves, thresholds inside and at
+the pool edge, tie-heavy rows that take its row-masked fallback next to
+rows that do not, subnormals / signed zeros, and the fp32 64-bit-key
+variant forced with BTK_XC=1.
+
+Reference: approx.py:208-282 (stage1 + topk_with_indices),
+exact.py:130-159 (canonical order).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2412_04358_b200 as btk
+from paper_2412_04358_b200 import _lib
+from oracle import bucketed_oracle as O
+from tests.special_inputs import TORCH, special, to_dtype
+
+pytestmark = pytest.mark.gpu
+
+_DTC = {"f32": _lib.BTK_F32, "bf16": _lib.BTK_BF16, "f16": _lib.BTK_F16}
+
+
+def _bits(t):
+    t = t.detach().cpu()
+    return t.view(torch.int32 if t.dtype == torch.float32 else torch.int16).numpy()
+
+
+def _family(m, n, k, b, kb, dn):
+    return _lib.load().btk_kernel_family(m, n, k, b, kb, _DTC[dn], _lib.BTK_INTERLEAVED, n)
+
+
+def _check(x32, dn, k, b, kb):
+    x = to_dtype(x32, dn).cuda()
+    r = btk.approx_topk(x, k, btk.BucketScheme(b, kb))
+    wv, wi = O.approx_topk(x32, k, b, kb)
+    np.testing.assert_array_equal(r.indices.cpu().numpy(), wi)
+    want = _bits(torch.from_numpy(np.asarray(wv, np.float64)).to(TORCH[dn]))
+    np.testing.assert_array_equal(_bits(r.values), want)
+
+
+def _rowmask(x, k, b, kb):
+    """Per-row verdict of the exchange (0 = handled in-cluster, < 0 =
+    fallback K2) read from a prepared op's workspace."""
+    m, n = x.shape
+    op = btk.ApproxTopK(m, n, k, btk.BucketScheme(b, kb), dtype=x.dtype, device=x.device)
+    op.launch(x)
+    torch.cuda.synchronize()
+    return op.ws[: 4 * m].view(torch.int32).cpu().numpy(), op
+
+
+# (m, n, k, b, kb): cfg5 rows, thresholds at 1/2, ~0.6, the whole pool, k_b 1/2/4
+SHAPES = [
+    (3, 1 << 20, 65536, 65536, 2),
+    (2, 262144, 20000, 16384, 2),
+    (3, 131072, 12000, 16384, 2),
+    (2, 262144, 32768, 16384, 2),   # k = the whole pool (select all)
+    (2, 262144, 9000, 32768, 1),
+    (2, 262144, 30000, 8192, 4),
+    (5, 524288, 30000, 32768, 1),
+]
+
+
+@pytest.mark.parametrize("dn", ["bf16", "f16"])
+def test_xchg_normal_and_ties(dn):
+    rng = np.random.default_rng(11)
+    for (m, n, k, b, kb) in SHAPES:
+        assert _family(m, n, k, b, kb, dn) == _lib.BTK_FAM_XCHG, (m, n, k, b, kb)
+        x32 = torch.from_numpy(rng.standard_normal((m, n), dtype=np.float32)).to(TORCH[dn]).float().numpy()
+        _check(x32, dn, k, b, kb)
+        ties = np.round(x32 * 4) / 4  # few distinct values: large equal-value groups
+        _check(ties, dn, k, b, kb)
+
+
+@pytest.mark.parametrize("dn", ["bf16", "f16"])
+def test_xchg_special_values(dn):
+    rng = np.random.default_rng(12)
+    for (m, n, k, b, kb) in SHAPES[:4]:
+        for kind in ("subnormal", "subnormal_ties", "pm0"):
+            _check(special(rng, kind, m, n, dn), dn, k, b, kb)
+
+
+@pytest.mark.parametrize("dn", ["bf16", "f16"])
+def test_xchg_fallback_rows_mixed(dn):
+    """Tie-heavy rows overflow an owner and take the row-masked K2; normal
+    rows in the same batch stay in-cluster; both are exact."""
+    rng = np.random.default_rng(13)
+    m, n, k, b, kb = 4, 262144, 20000, 16384, 2
+    x32 = torch.from_numpy(rng.standard_normal((m, n), dtype=np.float32)).to(TORCH[dn]).float().numpy()
+    x32[1] = 0.5          # one value everywhere: every key in one owner
+    x32[3, ::2] = -0.0    # half signed zeros, half normals
+    _check(x32, dn, k, b, kb)
+    mask, _ = _rowmask(to_dtype(x32, dn).cuda(), k, b, kb)
+    assert mask[0] == 0 and mask[2] == 0, mask
+    assert mask[1] < 0, mask
+
+
+def test_xchg_cfg5_rows_stay_in_cluster():
+    """N(0,1) cfg5 rows: no fallback (the splitter margins hold)."""
+    x = torch.randn(32, 1 << 20, device="cuda").to(torch.bfloat16)
+    mask, op = _rowmask(x, 65536, 65536, 2)
+    assert (mask == 0).all(), np.unique(mask, return_counts=True)
+    # and the outputs equal the chunked-pool path's on the same input
+    import os
+    os.environ["BTK_XC"] = "0"
+    try:
+        ref = btk.approx_topk(x, 65536, btk.BucketScheme(65536, 2))
+    finally:
+        del os.environ["BTK_XC"]
+    assert torch.equal(op.indices, ref.indices)
+    assert torch.equal(op.values.view(torch.int16), ref.values.view(torch.int16))
+
+
+def test_xchg_fp32_forced(monkeypatch):
+    """fp32 through the 64-bit-key variant (BTK_XC=1; not the default)."""
+    monkeypatch.setenv("BTK_XC", "1")
+    rng = np.random.default_rng(14)
+    for (m, n, k, b, kb) in [(3, 65536, 16384, 8192, 2), (2, 65536, 16384, 2048, 8), (3, 65536, 10000, 8192, 2)]:
+        assert _family(m, n, k, b, kb, "f32") == _lib.BTK_FAM_XCHG
+        x32 = rng.standard_normal((m, n), dtype=np.float32)
+        _check(x32, "f32", k, b, kb)
+        _check(special(rng, "pm0", m, n, "f32"), "f32", k, b, kb)

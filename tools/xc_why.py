@@ -1,0 +1,16 @@
+"""Fallback-row census of fused_xchg (rowmask reasons; development tool)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_2412_04358_b200 as btk
+from bench import CONFIGS
+for cfg in sys.argv[1:] or ["cfg5", "cfg2_kb2"]:
+    dt, m, n, k, b, kb, _, _ = CONFIGS[cfg]
+    m = min(m, 64)
+    tdt = {"f32": torch.float32, "bf16": torch.bfloat16}[dt]
+    x = torch.randn(m, n, device="cuda").to(tdt)
+    op = btk.ApproxTopK(m, n, k, btk.BucketScheme(b, kb), dtype=tdt, device="cuda")
+    op.launch(x); torch.cuda.synchronize()
+    rm = op.ws[: m * 4].view(torch.int32).cpu().numpy()
+    vals, cnts = np.unique(rm, return_counts=True)
+    print(cfg, dict(zip(vals.tolist(), cnts.tolist())))
