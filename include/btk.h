@@ -115,6 +115,13 @@ int btk_topk_with_indices(const void* values, const int64_t* labels, int dtype, 
                           int64_t c, int64_t k, void* out_vals, int64_t* out_idx, void* ws,
                           size_t ws_bytes, uint32_t* flag, void* stream);
 
+/* Recall counts of index rows (reference recall.py:203-218,
+ * empirical_recall_rows): hits[r] = number of the k entries of approx row r
+ * that occur among the k entries of truth row r (int64 indices, device
+ * memory; row r at approx_idx + r*approx_stride).  No workspace. */
+int btk_recall_hits(const int64_t* approx_idx, int64_t approx_stride, const int64_t* truth_idx,
+                    int64_t truth_stride, int64_t m, int64_t k, int32_t* hits, void* stream);
+
 /* Paper's total-bandwidth numerator (reference bench.py:138-159):
  * m * (n*vb + k*(vb + ib)). */
 int64_t btk_min_bytes(int64_t m, int64_t n, int64_t k, int64_t value_bytes, int64_t index_bytes);

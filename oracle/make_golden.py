@@ -266,8 +266,80 @@ def f64_cases() -> None:
     print("f64 cases done", flush=True)
 
 
+# Monte-Carlo recall configs: (n, k, b, kb, assignment, trials, seed)
+MC_CASES = [
+    (512, 32, 32, 1, "interleaved", 200, 9),
+    (2048, 64, 32, 2, "interleaved", 300, 3),
+    (1000, 50, 50, 2, "contiguous", 150, 4),
+    (4096, 256, 128, 4, "interleaved", 100, 5),
+    (64, 8, 1, 8, "interleaved", 50, 0),
+]
+# CLI argument sets whose stdout / CSV the GPU CLI must reproduce
+CLI_RUNS = [
+    ["run", "--n", "128", "--k", "8", "--b", "16", "--kb", "1", "--seed", "3"],
+    ["run", "--n", "1000", "--m", "3", "--k", "20", "--b", "10", "--kb", "3", "--seed", "7",
+     "--assignment", "contiguous"],
+    ["run", "--n", "4096", "--m", "2", "--k", "64", "--exact", "--seed", "11"],
+    ["run", "--n", "300", "--m", "2", "--k", "30", "--b", "7", "--kb", "5", "--seed", "1", "--mode", "auto"],
+]
+CLI_CORR = [
+    ["correlation", "--n", "512", "--k", "64", "--rho-list", "0.0,0.99", "--kb-list", "1,2,3",
+     "--trials", "200", "--shuffle", "--seed", "2"],
+]
+
+
+def recall_cli() -> None:
+    """Reference outputs for the recall loop and the CLI commands (run,
+    correlation) — the GPU versions must reproduce them exactly."""
+    import contextlib
+    import io
+    import json
+
+    approx, core, exact = _ref()
+    import bucketed_topk.cli as cli
+    import bucketed_topk.recall as recall
+
+    out = {"mc": [], "rows": None, "cli": [], "corr": []}
+    for n, k, b, kb, asg, trials, seed in MC_CASES:
+        A = core.Assignment.INTERLEAVED if asg == "interleaved" else core.Assignment.CONTIGUOUS
+        mc = recall.monte_carlo_recall(core.ProblemShape(m=1, n=n, k=k), core.BucketScheme(b=b, k_b=kb, assignment=A),
+                                       trials=trials, seed=seed, block_rows=64)
+        out["mc"].append({"n": n, "k": k, "b": b, "kb": kb, "asg": asg, "trials": trials, "seed": seed,
+                          "mean_recall": mc.mean_recall, "stderr": mc.stderr})
+        print("mc", n, k, b, kb, flush=True)
+    rng = np.random.default_rng(77)
+    x = rng.standard_normal((6, 2000))
+    got = approx.approx_topk(x, 40, core.BucketScheme(b=20, k_b=2))
+    want = exact.exact_topk_oracle(x, 40)
+    out["rows"] = {"seed": 77, "m": 6, "n": 2000, "k": 40, "b": 20, "kb": 2,
+                   "recall": recall.empirical_recall_rows(got, want).tolist()}
+    for argv in CLI_RUNS + CLI_CORR:
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            code = cli.main(list(argv))
+        (out["corr"] if argv[0] == "correlation" else out["cli"]).append(
+            {"argv": argv, "code": code, "stdout": buf.getvalue()})
+        print("cli", argv[0], flush=True)
+    import bucketed_topk.cost as cost
+    import bucketed_topk.simdata as simdata
+    out["derive_seed"] = [[sd, st, simdata.derive_seed(sd, st)] for sd, st in ((0, 0), (7, 3), (2**63 + 5, 1000))]
+    ar = simdata.ar1_batch(3, 257, 0.9, seed=4)
+    out["ar1"] = {"trials": 3, "n": 257, "rho": 0.9, "seed": 4, "sha": hashlib.sha256(ar.tobytes()).hexdigest()}
+    perm = simdata.permute(np.arange(50), seed=3, row=2)
+    out["permute"] = {"n": 50, "seed": 3, "row": 2, "out": perm.tolist()}
+    S = cost.CostModelKind.SERIAL
+    out["cost"] = [{"n": n, "k": k, "m": m, "b": b, "kb": kb, "exact": cost.exact_cost(S, n, k, m),
+                    "approx": cost.approx_cost(S, n, k, m, b, kb)}
+                   for n, k, m, b, kb in ((256, 16, 2, 16, 1), (65536, 64, 128, 64, 1), (4096, 64, 3, 16, 8))]
+    with open(os.path.join(OUT, "recall_cli.json"), "w") as fh:
+        json.dump(out, fh, indent=1)
+    print("recall/cli done", flush=True)
+
+
 if __name__ == "__main__":
-    if "--cfg5" in sys.argv:
+    if "--recall" in sys.argv:
+        recall_cli()
+    elif "--cfg5" in sys.argv:
         cfg5_rows()
     elif "--f64" in sys.argv:
         f64_cases()

@@ -15,6 +15,8 @@ from .exact import (ScoredIndex, TopKResult, exact_topk_oracle, priority_queue_t
 from .approx import (ApproxTopK, ChunkedMerge, ExecutionMode, PerBucket, Stage1Candidates,
                      approx_topk, select_mode, stage1)
 from .shard import approx_topk_sharded, distributed_approx_topk, row_blocks
+from .recall import MonteCarloRecall, empirical_recall, empirical_recall_rows, monte_carlo_recall
+from . import simdata
 
 __version__ = "0.1.0"
 
@@ -26,4 +28,5 @@ __all__ = [
     "ApproxTopK", "ChunkedMerge", "ExecutionMode", "PerBucket", "Stage1Candidates", "approx_topk",
     "select_mode", "stage1",
     "approx_topk_sharded", "distributed_approx_topk", "row_blocks",
+    "MonteCarloRecall", "empirical_recall", "empirical_recall_rows", "monte_carlo_recall", "simdata",
 ]

@@ -36,6 +36,7 @@ SIGNATURES = {
     "btk_exact_topk": (_i, [_vp, _i64, _i] + [_i64] * 3 + [_vp, _vp, _vp, _sz, _vp, _vp]),
     "btk_topk_with_indices_workspace_bytes": (_sz, [_i64] * 3 + [_i]),
     "btk_topk_with_indices": (_i, [_vp, _vp, _i] + [_i64] * 3 + [_vp, _vp, _vp, _sz, _vp, _vp]),
+    "btk_recall_hits": (_i, [_vp, _i64, _vp, _i64, _i64, _i64, _vp, _vp]),
     "btk_min_bytes": (_i64, [_i64] * 5),
     "btk_uses_fused_path": (_i, [_i64] * 5 + [_i, _i, _i64]),
     "btk_launch_count": (_i, [_i64] * 5 + [_i, _i, _i64]),
