@@ -100,6 +100,18 @@ int btk_stage1(const void* x, int64_t row_stride, int dtype, int64_t m, int64_t 
                int64_t kb, int layout, void* out_vals, int64_t* out_idx, void* ws,
                size_t ws_bytes, uint32_t* nonfinite_flag, void* stream);
 
+/* btk_approx_topk with launch flags.  BTK_INPUT_READY: the caller
+ * guarantees that `x` was not written by the work queued before this call
+ * on `stream` (e.g. independent batches resident in HBM).  The kernels then
+ * stream the input while the preceding kernel drains (programmatic
+ * dependent launch) and wait for it only before their first global write,
+ * so back-to-back launches overlap.  Results are identical either way. */
+enum btk_launch_flags { BTK_INPUT_READY = 1 };
+int btk_approx_topk_flags(const void* x, int64_t row_stride, int dtype, int64_t m, int64_t n,
+                          int64_t k, int64_t b, int64_t kb, int layout, void* out_vals,
+                          int64_t* out_idx, void* ws, size_t ws_bytes, uint32_t* nonfinite_flag,
+                          uint32_t flags, void* stream);
+
 /* Exact canonical top-k per row.  reference exact.py:162-173
  * (exact_topk_oracle); equals btk_approx_topk with b = 1, k_b = k. */
 size_t btk_exact_workspace_bytes(int64_t m, int64_t n, int64_t k, int dtype);

@@ -19,6 +19,7 @@ BTK_F32, BTK_BF16, BTK_F16, BTK_F64 = 0, 1, 2, 3
 (BTK_FAM_GENERIC, BTK_FAM_NARROW, BTK_FAM_WIDE, BTK_FAM_ROWS, BTK_FAM_VEC_POOL, BTK_FAM_MATERIALIZE,
  BTK_FAM_F64, BTK_FAM_POOL_CHUNKED, BTK_FAM_XCHG) = range(9)
 BTK_INTERLEAVED, BTK_CONTIGUOUS = 0, 1
+BTK_INPUT_READY = 1
 
 _i64, _sz, _vp, _i = ctypes.c_int64, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_int
 
@@ -30,6 +31,8 @@ SIGNATURES = {
     "btk_workspace_bytes": (_sz, [_i64] * 5 + [_i, _i]),
     "btk_plan_workspace_bytes": (_sz, [_vp, _i64, _i] + [_i64] * 5 + [_i]),
     "btk_approx_topk": (_i, [_vp, _i64, _i] + [_i64] * 5 + [_i, _vp, _vp, _vp, _sz, _vp, _vp]),
+    "btk_approx_topk_flags": (_i, [_vp, _i64, _i] + [_i64] * 5 + [_i, _vp, _vp, _vp, _sz, _vp,
+                                                               ctypes.c_uint32, _vp]),
     "btk_stage1_workspace_bytes": (_sz, [_i64] * 4 + [_i, _i]),
     "btk_stage1": (_i, [_vp, _i64, _i] + [_i64] * 4 + [_i, _vp, _vp, _vp, _sz, _vp, _vp]),
     "btk_exact_workspace_bytes": (_sz, [_i64] * 3 + [_i]),

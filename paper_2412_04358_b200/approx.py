@@ -100,7 +100,7 @@ class ApproxTopK:
     """
 
     def __init__(self, m: int, n: int, k: int, scheme: BucketScheme, dtype=torch.float32,
-                 device="cuda", row_stride: Optional[int] = None):
+                 device="cuda", row_stride: Optional[int] = None, inputs_ready: bool = False):
         check_parameters(m, n, k, scheme.b, scheme.k_b)
         self.m, self.n, self.k, self.scheme = m, n, k, scheme
         self.device = torch.device(device)
@@ -111,6 +111,12 @@ class ApproxTopK:
         self.lib = _lib.load()
         self.dt = _ops.dtype_code(torch.empty(0, dtype=dtype))
         self.layout = _layout(scheme.assignment)
+        # BTK_INPUT_READY (include/btk.h): the caller promises that inputs are
+        # never written by the work queued just before a launch (independent
+        # batches resident in HBM), so back-to-back launches may overlap: each
+        # streams its input while the previous one drains and waits for it
+        # only before writing.  Results are identical either way.
+        self.launch_flags = _lib.BTK_INPUT_READY if inputs_ready else 0
         with torch.cuda.device(self.device):
             self.values = torch.empty((m, k), dtype=dtype, device=self.device)
             self.indices = torch.empty((m, k), dtype=torch.int64, device=self.device)
@@ -137,10 +143,10 @@ class ApproxTopK:
         if x.data_ptr() % 16:
             raise ValueError("prepared ApproxTopK needs a 16-byte aligned input (use approx_topk "
                              "for arbitrary views)")
-        st = self.lib.btk_approx_topk(
+        st = self.lib.btk_approx_topk_flags(
             x.data_ptr(), self.row_stride, self.dt, self.m, self.n, self.k, self.scheme.b,
             self.scheme.k_b, self.layout, self.values.data_ptr(), self.indices.data_ptr(),
-            self.ws.data_ptr(), self.ws_bytes, self.flag.data_ptr(),
+            self.ws.data_ptr(), self.ws_bytes, self.flag.data_ptr(), self.launch_flags,
             _ops.stream_handle(self.device) if stream is None else stream)
         _ops.raise_status(st, "(approx_topk)")
 

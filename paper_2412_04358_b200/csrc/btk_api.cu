@@ -238,6 +238,13 @@ int btk_launch_count(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, int
 int btk_approx_topk(const void* x, int64_t row_stride, int dtype, int64_t m, int64_t n, int64_t k,
                     int64_t b, int64_t kb, int layout, void* out_vals, int64_t* out_idx, void* ws,
                     size_t ws_bytes, uint32_t* flag, void* stream) {
+  return btk_approx_topk_flags(x, row_stride, dtype, m, n, k, b, kb, layout, out_vals, out_idx, ws,
+                               ws_bytes, flag, 0u, stream);
+}
+
+int btk_approx_topk_flags(const void* x, int64_t row_stride, int dtype, int64_t m, int64_t n, int64_t k,
+                          int64_t b, int64_t kb, int layout, void* out_vals, int64_t* out_idx, void* ws,
+                          size_t ws_bytes, uint32_t* flag, uint32_t flags, void* stream) {
   int rc = btk_validate(m, n, k, b, kb);
   if (rc) return rc;
   rc = check_common(x, dtype, layout, n, row_stride);
@@ -257,6 +264,7 @@ int btk_approx_topk(const void* x, int64_t row_stride, int dtype, int64_t m, int
   p.layout = layout;
   p.geo = geo_for(dtype, n);
   p.flag = flag;
+  p.flags = flags & BTK_INPUT_READY;
   if (xchg_supported(p)) {
     const size_t need = xchg_workspace_bytes(p);
     if (ws_bytes < need || (reinterpret_cast<uintptr_t>(ws) & 255)) return BTK_ERR_WORKSPACE;

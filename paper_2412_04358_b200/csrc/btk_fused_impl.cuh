@@ -149,9 +149,15 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
 
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-// Outputs are written only after the predecessor grid completed (we already
-// waited before the first read, so this is a no-op kept as the hook).
-__device__ __forceinline__ void pdl_wait_writes() {}
+// Launch-order contract for global writes.  Normally a kernel waits for its
+// predecessor before its first input read (the predecessor may have
+// produced the input), so writes need nothing more.  With early reads
+// (BTK_INPUT_READY: the caller guarantees the input is not written by the
+// preceding work in the stream) the kernel streams its input while the
+// predecessor drains and waits only here, before its first global write.
+__device__ __forceinline__ void pdl_wait_writes(bool early) {
+  if (early) pdl_wait();
+}
 
 __device__ __forceinline__ uint4 ldg_stream(const void* p) {
   uint4 r;
@@ -273,11 +279,12 @@ __device__ __forceinline__ void emit_comp(uint64_t c, int64_t pos, const CompGeo
 template <int DT, int NT, int ITEMS>
 __device__ __forceinline__ void stage2_emit(uint64_t* pool, uint8_t* aux, int64_t P, int64_t k,
                                             int lognb, int64_t row, const CompGeo& geo,
-                                            void* out_vals, int64_t* out_idx, bool trace_on = false) {
+                                            void* out_vals, int64_t* out_idx, bool trace_on = false,
+                                            bool early = false) {
   if constexpr (ITEMS == 0) {
     // P <= 64: every key counts the keys above it (broadcast smem reads;
     // composite keys are unique) and writes itself at that rank — no sort
-    pdl_wait_writes();
+    pdl_wait_writes(early);
     for (int p = threadIdx.x; p < (int)P; p += NT) {
       const uint64_t x = pool[p];
       if (!x) continue;  // empty slot
@@ -292,7 +299,7 @@ __device__ __forceinline__ void stage2_emit(uint64_t* pool, uint8_t* aux, int64_
     const RankSmem S = rank_smem(pool, aux, P, k, lognb, NT);
     rank_select_sort<DT, NT, ITEMS>(S, (int)P, (int)k, lognb, geo.ib);
     if (trace_on && threadIdx.x == 0 && blockIdx.x < 8192) g_trace[blockIdx.x][5] = gtime();
-    pdl_wait_writes();
+    pdl_wait_writes(early);
     for (int64_t q = threadIdx.x; q < k; q += NT)
       emit_comp<DT>(rs_key(pool, S.inv[q]), row * k + q, geo, out_vals, out_idx);
   }
@@ -571,6 +578,7 @@ struct NarrowArgs {
   int64_t* out_idx;
   uint32_t* flag;
   int trace;
+  int early;  // read the input before the predecessor completes (BTK_INPUT_READY)
 };
 
 template <int KB>
@@ -645,7 +653,7 @@ __device__ __forceinline__ void narrow_tail(const NarrowArgs& a, uint8_t* smem, 
     g_trace[blockIdx.x][6] = smid;
   }
   stage2_emit<DT, NT, ITEMS>(pool, smem + a.aux_off, a.P, a.k, a.lognb, row, a.geo, a.out_vals,
-                            a.out_idx, a.trace != 0);
+                            a.out_idx, a.trace != 0, a.early != 0);
   if (tr) g_trace[blockIdx.x][4] = gtime();}
 
 template <int DT, int KB, int NT, int ITEMS>
@@ -684,7 +692,7 @@ __global__ void __launch_bounds__(NT) fused_narrow(NarrowArgs a) {
   // resident during our tail, and wait for our predecessor to finish (its
   // writes may be our input) before the first read.
   pdl_trigger();
-  pdl_wait();
+  if (!a.early) pdl_wait();
   __syncthreads();
 
   uint64_t policy = 0;
@@ -777,6 +785,7 @@ struct RowsArgs {
   void* out_vals;
   int64_t* out_idx;
   uint32_t* flag;
+  int early;  // read the input before the predecessor completes (BTK_INPUT_READY)
 };
 
 template <int DT, int KB, int GPL, int U, int ITEMS>
@@ -794,7 +803,7 @@ __global__ void __launch_bounds__(256, ROWS_MINB) fused_rows(RowsArgs a) {
   const int G = a.G;
   uint32_t bad = 0;
   pdl_trigger();
-  pdl_wait();
+  if (!a.early) pdl_wait();
   for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < a.m; row += (int64_t)gridDim.x * 8) {
     const uint8_t* rowp = static_cast<const uint8_t*>(a.x) + row * a.row_stride * ESZ;
     Scanner<DT, KB> sc[GPL];
@@ -840,6 +849,7 @@ __global__ void __launch_bounds__(256, ROWS_MINB) fused_rows(RowsArgs a) {
     }
     __syncwarp();
     warp_rank_sort<DT, ITEMS>(pool, (int)a.P, (int)a.k, inv, bid, hist, a.lognb, a.geo.ib);
+    pdl_wait_writes(a.early != 0);
     for (int64_t q = lane; q < a.k; q += 32)
       emit_comp<DT>(rs_key(pool, inv[q]), row * a.k + q, a.geo, a.out_vals, a.out_idx);
     __syncwarp();
@@ -862,6 +872,7 @@ struct WideArgs {
   int64_t* out_idx;
   uint32_t* flag;
   int trace;
+  int early;  // read the input before the predecessor completes (BTK_INPUT_READY)
 };
 
 template <int DT, int KB, int NT, int U, int ITEMS>
@@ -876,7 +887,7 @@ __global__ void __launch_bounds__(NT, 1) fused_wide(WideArgs a) {
   const int tid = threadIdx.x;
   uint32_t bad = 0;
   pdl_trigger();
-  pdl_wait();
+  if (!a.early) pdl_wait();
   const bool tr = a.trace && tid == 0 && blockIdx.x < 8192;
   if (tr) g_trace[blockIdx.x][0] = gtime();
   for (int64_t g = tid; g < a.G; g += NT) {
@@ -915,7 +926,7 @@ __global__ void __launch_bounds__(NT, 1) fused_wide(WideArgs a) {
   if (tr) g_trace[blockIdx.x][2] = g_trace[blockIdx.x][3] = gtime();
   if (__syncthreads_or(nonfinite_hit<DT>(bad)) && tid == 0 && a.flag) atomicOr(a.flag, 1u);
   stage2_emit<DT, NT, ITEMS>(pool, smem + a.aux_off, a.P, a.k, a.lognb, row, a.geo, a.out_vals,
-                            a.out_idx, a.trace != 0);
+                            a.out_idx, a.trace != 0, a.early != 0);
   if (tr) g_trace[blockIdx.x][4] = gtime();
 }
 
@@ -1088,6 +1099,7 @@ inline bool plan_narrow(const Problem& p, Plan& pl) {
   a.geo = p.geo;
   a.flag = p.flag;
   a.trace = env_int("BTK_TRACE", 0);
+  a.early = (p.flags & 1u) && pdl_enabled() ? 1 : 0;
   pl.kind = NARROW;
   pl.nt = NT;
   pl.smem = smem;
@@ -1111,6 +1123,7 @@ inline bool plan_wide(const Problem& p, Plan& pl) {
   a.geo = p.geo;
   a.flag = p.flag;
   a.trace = env_int("BTK_TRACE", 0);
+  a.early = (p.flags & 1u) && pdl_enabled() ? 1 : 0;
   pl.smem = stage2_bytes(P, p.k, WIDE_NT);
   pl.kind = WIDE;
   pl.nt = WIDE_NT;
@@ -1140,6 +1153,7 @@ inline bool plan_rows(const Problem& p, Plan& pl) {
   pl.rows_items = P <= 256 ? 8 : (P <= 512 ? 16 : 32);
   a.geo = p.geo;
   a.flag = p.flag;
+  a.early = (p.flags & 1u) && pdl_enabled() ? 1 : 0;
   pl.kind = ROWS;
   pl.nt = 256;
   pl.smem = smem;
@@ -1230,8 +1244,17 @@ cudaError_t launch_rows_t(const Plan& pl, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   const int64_t want = (pl.ra.m + 7) / 8;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)std::max(1, per_sm) * num_sms()));
-  kern<<<grid, pl.nt, pl.smem, st>>>(pl.ra);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(pl.nt);
+  cfg.dynamicSmemBytes = pl.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, pl.ra);
 }
 
 template <int DT, int KB>

@@ -81,6 +81,7 @@ struct Problem {
   int layout;          // 0 interleaved, 1 contiguous
   CompGeo geo;
   uint32_t* flag;      // device non-finite flag (may be null)
+  uint32_t flags = 0;  // BTK_INPUT_READY: input not produced by the preceding stream work
 };
 
 // Generic stage 1, k_b <= 16: one thread per (row, bucket), register queue.

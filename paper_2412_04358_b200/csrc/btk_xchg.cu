@@ -105,6 +105,7 @@ struct XArgs {
   int* rowmask;    // per row: 0 handled here, -1 generic fallback
   uint64_t* pool;  // fallback rows: m x (b*k_b) comps, bucket-major (s1_vec layout)
   int trace;       // development timeline (BTK_XC_TRACE=1): globaltimer per CTA and phase
+  int early;       // read the input before the predecessor completes (BTK_INPUT_READY)
 };
 
 constexpr int TRACE_CTAS = 16384;
@@ -263,7 +264,7 @@ __global__ void __launch_bounds__(NT, 2) fused_xchg(XArgs a) {
   if (tid < C) { tot[tid] = 0u; dbase[tid] = 0u; }
   __syncthreads();
   pdl_trigger();
-  pdl_wait();
+  if (!a.early) pdl_wait();
   mark(a, 0);
 
   // ---------------------------------------------------------------- 1. stage 1
@@ -457,6 +458,7 @@ __global__ void __launch_bounds__(NT, 2) fused_xchg(XArgs a) {
   __syncthreads();
   const int64_t start = (int64_t)s_start;
   const int R = (int)tot[rank];
+  pdl_wait_writes(a.early != 0);  // first global writes below
   if (s_why) {  // identical verdict in every CTA (same splitters, same totals)
     if (rank == 0 && tid == 0) a.rowmask[row] = -1 - s_why;
     uint64_t* dst = a.pool + row * a.b * KB + col0 * KB;
@@ -693,6 +695,7 @@ cudaError_t run_xchg(const Problem& p, void* ws, void* out_vals, int64_t* out_id
   a.rowmask = rowmask;
   a.pool = pool;
   a.trace = fz::env_int("BTK_XC_TRACE", 0);
+  a.early = (p.flags & 1u) && fz::pdl_enabled() ? 1 : 0;
   cudaError_t e = cudaErrorInvalidValue;
   switch (p.dtype) {
     case F32: e = xc::launch_dt<F32>(a, p.kb, st); break;

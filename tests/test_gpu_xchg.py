@@ -121,3 +121,43 @@ def test_xchg_fp32_forced(monkeypatch):
         x32 = rng.standard_normal((m, n), dtype=np.float32)
         _check(x32, "f32", k, b, kb)
         _check(special(rng, "pm0", m, n, "f32"), "f32", k, b, kb)
+
+
+@pytest.mark.parametrize("shape", [
+    (3, 65536, 64, 64, 1, torch.float32),          # fused_narrow (cluster, TMA ring)
+    (1200, 2048, 64, 64, 1, torch.bfloat16),       # fused_rows (one warp per row)
+    (2, 65536, 16384, 8192, 2, torch.float32),     # fused_wide
+    (2, 262144, 20000, 16384, 2, torch.bfloat16),  # fused_xchg
+], ids=["narrow", "rows", "wide", "xchg"])
+def test_inputs_ready_overlapped_launches_equal_serial(shape):
+    """BTK_INPUT_READY launches back to back (eager and in a CUDA graph)
+    over rotating buffers: every step's outputs equal the conservative
+    launch's, and the last write wins (writes still wait for the
+    predecessor)."""
+    m, n, k, b, kb, dt = shape
+    xs = [torch.randn(m, n, device="cuda").to(dt) for _ in range(3)]
+    sch = btk.BucketScheme(b, kb)
+    ready = btk.ApproxTopK(m, n, k, sch, dtype=dt, device="cuda", inputs_ready=True)
+    dep = btk.ApproxTopK(m, n, k, sch, dtype=dt, device="cuda")
+    want = []
+    for x in xs:
+        dep.launch(x)
+        want.append((dep.values.clone(), dep.indices.clone()))
+    got = []
+    for i in range(7):
+        ready.launch(xs[i % 3])
+        got.append((ready.values.clone(), ready.indices.clone()))
+    torch.cuda.synchronize()
+    for i, (v, ix) in enumerate(got):
+        assert torch.equal(ix, want[i % 3][1]) and torch.equal(v, want[i % 3][0]), i
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ready.launch(xs[0])
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for i in range(5):
+                ready.launch(xs[i % 3])
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(ready.indices, want[4 % 3][1]) and torch.equal(ready.values, want[4 % 3][0])
