@@ -334,7 +334,6 @@ __global__ void __launch_bounds__(NT) f64_lsd(K128* A, K128* B, int64_t kk, Out 
   __shared__ uint32_t ghist[256];
   __shared__ uint32_t runbase[256];
   __shared__ uint32_t whist[NW][256];
-  __shared__ int s_skip;
   const int64_t s = blockIdx.x;
   K128* src = A + s * kk;
   K128* dst = B + s * kk;
@@ -342,11 +341,12 @@ __global__ void __launch_bounds__(NT) f64_lsd(K128* A, K128* B, int64_t kk, Out 
   const uint32_t lt = lanemask_lt();
   for (int shift = 0; shift < 128; shift += 8) {
     for (int j = threadIdx.x; j < 256; j += NT) ghist[j] = 0;
-    if (threadIdx.x == 0) s_skip = 0;
     __syncthreads();
     for (int64_t p = threadIdx.x; p < kk; p += NT) atomicAdd(&ghist[255u - digit(src[p], shift)], 1u);
     __syncthreads();
-    if (threadIdx.x < 256 && ghist[threadIdx.x] == (uint32_t)kk) s_skip = 1;
+    // block-uniform skip verdict (no shared flag: a reset by thread 0 at the
+    // next pass would race with the readers of this one)
+    const bool full = threadIdx.x < 256 && ghist[threadIdx.x] == (uint32_t)kk;
     if (warp == 0) {  // exclusive scan of ghist -> runbase
       uint32_t v[8], sum = 0;
 #pragma unroll
@@ -361,8 +361,7 @@ __global__ void __launch_bounds__(NT) f64_lsd(K128* A, K128* B, int64_t kk, Out 
 #pragma unroll
       for (int q = 0; q < 8; ++q) { runbase[lane * 8 + q] = run; run += v[q]; }
     }
-    __syncthreads();
-    if (s_skip) continue;
+    if (__syncthreads_or(full)) continue;
     for (int64_t t0 = 0; t0 < kk; t0 += NT) {
       const int64_t p = t0 + threadIdx.x;
       const bool valid = p < kk;

@@ -140,7 +140,6 @@ __global__ void __launch_bounds__(NT) k2_global_lsd(uint64_t* __restrict__ A, ui
   __shared__ uint32_t dtotal[RADIX];
   __shared__ uint32_t runbase[RADIX];
   __shared__ uint32_t ghist[RADIX];
-  __shared__ int s_skip;
   const int64_t seg = blockIdx.x;
   if (mask && mask[seg * mask_stride] >= 0) return;
   uint64_t* src = A + seg * stride_a;
@@ -148,14 +147,14 @@ __global__ void __launch_bounds__(NT) k2_global_lsd(uint64_t* __restrict__ A, ui
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int shift = 1; shift < g.nbits; shift += 8) {
     for (int j = threadIdx.x; j < RADIX; j += NT) ghist[j] = 0;
-    if (threadIdx.x == 0) s_skip = 0;
     __syncthreads();
     for (int64_t p = threadIdx.x; p < kk; p += NT) atomicAdd(&ghist[desc_digit(src[p], shift)], 1u);
     __syncthreads();
-    if (threadIdx.x < RADIX && ghist[threadIdx.x] == (uint32_t)kk) s_skip = 1;
+    const bool full = threadIdx.x < RADIX && ghist[threadIdx.x] == (uint32_t)kk;
     if (warp == 0) warp_exscan256(ghist, runbase);
-    __syncthreads();
-    if (s_skip) continue;
+    // a digit constant over the segment: identity pass (block-uniform verdict;
+    // a shared flag reset by thread 0 at the next pass raced with its readers)
+    if (__syncthreads_or(full)) continue;
     for (int64_t t0 = 0; t0 < kk; t0 += N) {
       uint64_t key[ITEMS];
       uint32_t rank[ITEMS];

@@ -263,6 +263,9 @@ __global__ void __launch_bounds__(NT, 2) fused_xchg(XArgs a) {
   if (tid == 0) { s_max = 0ull; s_min = ~0ull; s_vary = 0ull; }
   if (tid < C) { tot[tid] = 0u; dbase[tid] = 0u; }
   __syncthreads();
+  // every CTA of the cluster must have started before any DSMEM access: arrive
+  // now, wait right before the first remote store (stage 1 hides the latency)
+  cluster_arrive_release();
   pdl_trigger();
   if (!a.early) pdl_wait();
   mark(a, 0);
@@ -344,6 +347,7 @@ __global__ void __launch_bounds__(NT, 2) fused_xchg(XArgs a) {
       srt[r] = x;
     }
     __syncthreads();
+    cluster_wait_acquire();  // all peers resident (matches the arrive above)
     if (tid <= C) {  // local estimate of splitter tid, stored into every CTA
       uint64_t v;
       if (tid == 0) v = s_max;
