@@ -44,9 +44,12 @@ CONFIGS = {
     "cfg3_r4": ("bf16", 128, 1 << 20, 256, 1024, 1, "weak", "cfg3: bf16 m=128 n=2^20 k=256 b=1024 k_b=1"),
     "cfg3_r8": ("bf16", 128, 1 << 20, 256, 2048, 1, "weak", "cfg3: bf16 m=128 n=2^20 k=256 b=2048 k_b=1"),
     "cfg4": ("bf16", 4096, 32768, 512, 512, 1, "weak", "cfg4: bf16 m=4096 n=32768 k=512 b=512 k_b=1"),
+    "cfg3c_r2": ("bf16", 128, 1 << 20, 256, 512, 1, "weak",
+                 "cfg3 with contiguous buckets: bf16 m=128 n=2^20 k=256 b=512 k_b=1 contiguous"),
     "cfg5": ("bf16", 8192, 1 << 20, 65536, 65536, 2, "strong",
              "cfg5: bf16 m=8192 n=2^20 k=65536 b=65536 k_b=2 (ratio 2), rows sharded over GPUs"),
 }
+CONTIGUOUS = {"cfg3c_r2"}  # configs with contiguous buckets (the rest interleaved)
 L2_BYTES = 126 * 2**20
 FALLBACK_HBM_GBS = 6650.0
 
@@ -145,7 +148,7 @@ def workload_config(cfg: str, world: int) -> dict:
     m_local, m_total = rows_for(cfg, world, 0)
     nbuf = n_buffers(m_local * n * vb)
     return {"workload": desc, "rows_per_gpu": m_local, "rows_total": m_total, "n": n, "k": k,
-            "b": b, "k_b": kb, "assignment": "interleaved",
+            "b": b, "k_b": kb, "assignment": "contiguous" if cfg in CONTIGUOUS else "interleaved",
             "l2": f"inputs larger than L2: {nbuf} rotating input buffers of {m_local * n * vb / 2**20:.1f} MiB "
                   f"per GPU (> 4 x {L2_BYTES // 2**20} MiB L2)"}
 
@@ -161,15 +164,15 @@ def reference_impl():
             from bucketed_topk.approx import approx_topk as ref_approx
             from bucketed_topk.core import Assignment as RA, BucketScheme as RB
 
-            def run(x, k, b, kb, workers):
-                return ref_approx(x, k, RB(b=b, k_b=kb, assignment=RA.INTERLEAVED), workers=workers)
+            def run(x, k, b, kb, workers, asg="interleaved"):
+                return ref_approx(x, k, RB(b=b, k_b=kb, assignment=RA(asg)), workers=workers)
             return run, "reference", "bucketed_topk.approx.approx_topk (unmodified reference, baseline/_ref)"
         except Exception:
             pass
     from oracle import bucketed_oracle as O
 
-    def run(x, k, b, kb, workers):
-        return O.approx_topk(x, k, b, kb, workers=workers)
+    def run(x, k, b, kb, workers, asg="interleaved"):
+        return O.approx_topk(x, k, b, kb, asg, workers=workers)
     return run, "port", "oracle/bucketed_oracle.approx_topk (NumPy port of the reference)"
 
 
@@ -198,9 +201,10 @@ def cpu_time(cfg, steps, warmup, budget_s):
             x = (((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint32) << 16).view(np.float32)
         return x.astype(np.float64)  # the reference computes in float64 (exact upcast)
 
+    asg = "contiguous" if cfg in CONTIGUOUS else "interleaved"
     x = gen(rows)
     t0 = time.perf_counter()
-    run(x, k, b, kb, cores)
+    run(x, k, b, kb, cores, asg)
     t1 = time.perf_counter() - t0
     per_call = budget_s / max(1, steps + warmup)
     if t1 > per_call and rows > 1:
@@ -208,12 +212,12 @@ def cpu_time(cfg, steps, warmup, budget_s):
         x = gen(rows)
     bufs = [x, gen(rows)]
     for i in range(warmup):
-        run(bufs[i % 2], k, b, kb, cores)
+        run(bufs[i % 2], k, b, kb, cores, asg)
     times = []
     for i in range(steps):
         xi = bufs[i % 2]
         a = time.perf_counter()
-        run(xi, k, b, kb, cores)
+        run(xi, k, b, kb, cores, asg)
         times.append(time.perf_counter() - a)
     mean = statistics.mean(times)
     sem = (statistics.stdev(times) / len(times) ** 0.5 / mean) if len(times) > 1 else None
@@ -429,7 +433,7 @@ def main():
     tdt = {"f32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16}[dt]
     vb = 4 if dt == "f32" else 2
     m_local, m_total = rows_for(cfg, world, rank)
-    scheme = btk.BucketScheme(b, kb, btk.Assignment.INTERLEAVED)
+    scheme = btk.BucketScheme(b, kb, btk.Assignment.CONTIGUOUS if cfg in CONTIGUOUS else btk.Assignment.INTERLEAVED)
     batch_bytes = m_local * n * vb
     nbuf = n_buffers(batch_bytes)
     free = torch.cuda.mem_get_info(dev)[0]

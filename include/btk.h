@@ -153,7 +153,8 @@ enum btk_family {
   BTK_FAM_MATERIALIZE = 5, /* every element materialised + K2 (b == 1, k_b > 16) */
   BTK_FAM_F64 = 6,         /* float64: 128-bit keys (btk_f64.cu) */
   BTK_FAM_POOL_CHUNKED = 7, /* s1_vec pool + histogram-chunked Stage 2 (btk_pool.cu) */
-  BTK_FAM_XCHG = 8          /* fused_xchg: cluster per row, DSMEM value-range exchange (btk_xchg.cu) */
+  BTK_FAM_XCHG = 8,         /* fused_xchg: cluster per row, DSMEM value-range exchange (btk_xchg.cu) */
+  BTK_FAM_CONTIG = 9        /* s1_contig (contiguous layout, warp per bucket, 128-bit loads) + K2 */
 };
 int btk_kernel_family(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, int dtype,
                       int layout, int64_t row_stride);

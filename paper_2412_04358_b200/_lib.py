@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("BTK_LIB") or os.path.join(_HERE, "libbtk.so")
 
 BTK_F32, BTK_BF16, BTK_F16, BTK_F64 = 0, 1, 2, 3
 (BTK_FAM_GENERIC, BTK_FAM_NARROW, BTK_FAM_WIDE, BTK_FAM_ROWS, BTK_FAM_VEC_POOL, BTK_FAM_MATERIALIZE,
- BTK_FAM_F64, BTK_FAM_POOL_CHUNKED, BTK_FAM_XCHG) = range(9)
+ BTK_FAM_F64, BTK_FAM_POOL_CHUNKED, BTK_FAM_XCHG, BTK_FAM_CONTIG) = range(10)
 BTK_INTERLEAVED, BTK_CONTIGUOUS = 0, 1
 BTK_INPUT_READY = 1
 

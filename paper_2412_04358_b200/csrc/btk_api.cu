@@ -81,6 +81,7 @@ struct Carve {
 // Stage 1 into the bucket-major pool (m x b*kb comps).
 int stage1_pool(const Problem& p, const Plan& pl, Carve& cv, uint64_t* pool, cudaStream_t st) {
   if (stage1_vec_supported(p)) return cuda_status(run_stage1_vec(p, pool, st));
+  if (stage1_contig_supported(p)) return cuda_status(run_stage1_contig(p, pool, st));
   if (p.kb <= 16) return cuda_status(run_stage1_generic(p, pool, st));
   uint64_t* mat = cv.take(pl.mat);
   uint64_t* s1a = cv.take(pl.s1a);
@@ -200,6 +201,7 @@ int btk_kernel_family(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, in
   const int fk = fused_kind(p);
   if (fk) return fk;  // BTK_FAM_NARROW / WIDE / ROWS
   if (b == 1 || kb > 16) return BTK_FAM_MATERIALIZE;
+  if (stage1_contig_supported(p)) return BTK_FAM_CONTIG;
   if (pool_chunked_ok(p)) return BTK_FAM_POOL_CHUNKED;
   return stage1_vec_supported(p) ? BTK_FAM_VEC_POOL : BTK_FAM_GENERIC;
 }

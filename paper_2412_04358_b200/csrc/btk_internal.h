@@ -87,6 +87,10 @@ struct Problem {
 // Generic stage 1, k_b <= 16: one thread per (row, bucket), register queue.
 // pool: m x (b*kb) comps, bucket-major, sorted within bucket, 0 = empty.
 cudaError_t run_stage1_generic(const Problem& p, uint64_t* pool, cudaStream_t st);
+// Contiguous layout, k_b <= 8: one warp per (row, bucket), 128-bit loads
+// of the dense slice, warp merge of the lanes' queues.  Same pool layout.
+bool stage1_contig_supported(const Problem& p);
+cudaError_t run_stage1_contig(const Problem& p, uint64_t* pool, cudaStream_t st);
 // Vectorised stage 1 into the same pool (interleaved, k_b in {1,2,4,8},
 // V*k_b <= 16, 16-byte aligned rows); cudaErrorNotSupported otherwise.
 bool stage1_vec_supported(const Problem& p);

@@ -10,7 +10,7 @@
 // This is the universal path (contiguous layout, ragged shapes, odd
 // strides).  Interleaved shapes inside the fused envelope take
 // btk_fused.cu instead.
-#include "btk_internal.h"
+#include "btk_fused_impl.cuh"  // Queue, vector loads and unpacking (namespace fz)
 
 namespace btk {
 
@@ -113,6 +113,128 @@ __global__ void s1_emit(Problem p, const uint64_t* __restrict__ pool, int64_t C,
     store_bits<DT>(out_vals, row * C + off + qq, bits);
     out_idx[row * C + off + qq] = idx;
   }
+}
+
+// ---------------------------------------------------------------------------
+// Contiguous layout (bucket j = [ceil(jn/b), ceil((j+1)n/b)), reference
+// core.py:124-147, approx.py:121-124): a bucket is a dense slice, so one
+// WARP owns one (row, bucket).  Lane l streams vectors l, l+32, ... of the
+// slice with 128-bit loads (coalesced: a warp instruction reads 512
+// consecutive bytes), keeping a register queue of its top k_b (strict ">"
+// in increasing index order = first maximum); the 32 queues then merge by
+// k_b rounds of a warp max over composite keys (unique, canonical order).
+// Slices that do not start/end on a 16-byte boundary take scalar loads.
+template <int DT, int KB>
+__global__ void __launch_bounds__(256) s1_contig(Problem p, uint64_t* __restrict__ pool, int G) {
+  constexpr int V = 16 / (VT<DT>::W / 8);
+  constexpr int ESZ = VT<DT>::W / 8;
+  constexpr int U = 8;  // vectors in flight per lane
+  const int lane = threadIdx.x & 31, gl = lane % G, per_warp = 32 / G;
+  const int64_t P = p.b * p.kb;
+  const int64_t tasks = p.m * p.b;
+  uint32_t bad = 0;
+  for (int64_t t0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * per_warp; t0 < tasks;
+       t0 += (int64_t)gridDim.x * 8 * per_warp) {
+    const int64_t task = t0 + lane / G;  // this lane group's (row, bucket)
+    uint64_t best[KB];  // this lane's top k_b composite keys, descending
+#pragma unroll
+    for (int z = 0; z < KB; ++z) best[z] = 0ull;
+    int64_t row = 0, j = 0;
+    if (task < tasks) {
+      row = task / p.b;
+      j = task - row * p.b;
+      int64_t start, size, step;
+      bucket_span(p, j, start, size, step);
+      const uint8_t* xr = static_cast<const uint8_t*>(p.x) + row * p.row_stride * ESZ;
+      const bool vec = ((reinterpret_cast<uintptr_t>(xr) + start * ESZ) & 15) == 0 && (size % V) == 0 &&
+                       size / V < 0xFFFF;
+      if (vec) {
+        // the lane's vectors as V sub-streams (one per element slot), each
+        // with the packed / float queue of the fused scanners; the code of a
+        // vector is its ordinal in the slice, so idx = start + code*V + slot
+        const int64_t nv = size / V;
+        const uint8_t* base = xr + start * ESZ;
+        fz::Scanner<DT, KB> sc;
+        sc.init();
+        for (int64_t v0 = gl; v0 < nv; v0 += (int64_t)G * U) {
+          uint4 w[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            w[u] = (v0 + G * u < nv) ? fz::ldg_stream(base + (v0 + G * u) * 16) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (v0 + G * u < nv) sc.row(w[u], (int)(v0 + G * u));
+        }
+        bad |= sc.nonfinite() ? 1u : 0u;
+        sc.each_comp(0, V, start / V, p.geo, [&](int64_t, int, uint64_t c) { fz::comp_push<KB>(best, c); });
+      } else {
+        fz::Queue<KB> q;
+        q.init();
+        for (int64_t t = gl; t < size; t += G) {
+          const uint32_t bits = load_bits<DT>(xr, start + t);
+          bad |= nonfinite<DT>(bits) ? 1u : 0u;
+          float f;
+          if constexpr (DT == F32) f = __uint_as_float(bits);
+          else if constexpr (DT == BF16) f = __uint_as_float(bits << 16);
+          else f = __half2float(__ushort_as_half((unsigned short)bits));
+          q.push(f, (int)(start + t));
+        }
+#pragma unroll
+        for (int z = 0; z < KB; ++z) best[z] = fz::comp_of<DT>(q.v[z], q.t[z], 0, 1, p.geo);  // idx = t
+      }
+    }
+    // group merge: k_b rounds of a max over the group lanes' heads (xor
+    // offsets < G stay inside the aligned group)
+    int head = 0;
+#pragma unroll
+    for (int z = 0; z < KB; ++z) {
+      uint64_t mine = 0ull;
+#pragma unroll
+      for (int i = 0; i < KB; ++i) mine = (i == head) ? best[i] : mine;
+      uint64_t top = mine;
+      for (int o = G >> 1; o; o >>= 1) {
+        const uint64_t other = __shfl_xor_sync(0xFFFFFFFFu, top, o);
+        top = other > top ? other : top;
+      }
+      if (top != 0ull && mine == top) ++head;  // comps are unique: one owner
+      if (gl == 0 && task < tasks && z < p.kb) pool[row * P + j * p.kb + z] = top;
+    }
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0 && p.flag) atomicOr(p.flag, 1u);
+}
+
+template <int DT, int KB>
+static cudaError_t launch_contig(const Problem& p, uint64_t* pool, cudaStream_t st) {
+  // lanes per bucket: enough that each lane streams >= 16 vectors of it
+  const int V = 16 / (VT<DT>::W / 8);
+  const int64_t nv = (p.n / p.b) / V;
+  int G = 1;
+  while (G < 32 && nv / (2 * G) >= 16) G *= 2;
+  const int64_t blocks = (p.m * p.b + 8 * (32 / G) - 1) / (8 * (32 / G));
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 16));
+  s1_contig<DT, KB><<<grid, 256, 0, st>>>(p, pool, G);
+  return cudaGetLastError();
+}
+
+template <int DT>
+static cudaError_t contig_t(const Problem& p, uint64_t* pool, cudaStream_t st) {
+  if (p.kb <= 1) return launch_contig<DT, 1>(p, pool, st);
+  if (p.kb <= 2) return launch_contig<DT, 2>(p, pool, st);
+  if (p.kb <= 4) return launch_contig<DT, 4>(p, pool, st);
+  if (p.kb <= 8) return launch_contig<DT, 8>(p, pool, st);
+  return cudaErrorInvalidValue;
+}
+
+bool stage1_contig_supported(const Problem& p) { return p.layout == 1 && p.kb <= 8; }
+
+cudaError_t run_stage1_contig(const Problem& p, uint64_t* pool, cudaStream_t st) {
+  if (!stage1_contig_supported(p)) return cudaErrorNotSupported;
+  switch (p.dtype) {
+    case F32: return contig_t<F32>(p, pool, st);
+    case BF16: return contig_t<BF16>(p, pool, st);
+    case F16: return contig_t<F16>(p, pool, st);
+  }
+  return cudaErrorInvalidValue;
 }
 
 // ---------------------------------------------------------------------------

@@ -103,9 +103,9 @@ def test_every_family_special_values(dn):
         assert family(m, n, k, b, kb, dn) == fam, (fam, dn)
         for kind in KINDS:
             check(special(rng, kind, m, n, dn), dn, k, b, kb)
-    # contiguous layout (generic family)
+    # contiguous layout (warp-per-bucket family)
     m, n, k, b, kb = 2, 20000, 512, 256, 2
-    assert family(m, n, k, b, kb, dn, _lib.BTK_CONTIGUOUS) == 0
+    assert family(m, n, k, b, kb, dn, _lib.BTK_CONTIGUOUS) == _lib.BTK_FAM_CONTIG
     for kind in KINDS:
         check(special(rng, kind, m, n, dn), dn, k, b, kb, btk.Assignment.CONTIGUOUS)
 
