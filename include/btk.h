@@ -150,7 +150,8 @@ enum btk_family {
   BTK_FAM_WIDE = 2,        /* fused_wide: one CTA per row, LDG vector columns */
   BTK_FAM_ROWS = 3,        /* fused_rows: one warp per row */
   BTK_FAM_VEC_POOL = 4,    /* s1_vec pool + K2 */
-  BTK_FAM_MATERIALIZE = 5, /* every element materialised + K2 (b == 1, k_b > 16) */
+  BTK_FAM_MATERIALIZE = 5, /* b == 1 or k_b > 16: exact radix select per bucket straight from the
+                              scores (nothing materialised; name kept for ABI stability) + K2 */
   BTK_FAM_F64 = 6,         /* float64: 128-bit keys (btk_f64.cu) */
   BTK_FAM_POOL_CHUNKED = 7, /* s1_vec pool + histogram-chunked Stage 2 (btk_pool.cu) */
   BTK_FAM_XCHG = 8,         /* fused_xchg: cluster per row, DSMEM value-range exchange (btk_xchg.cu) */

@@ -41,18 +41,25 @@ struct Plan {
 
 Plan plan_generic(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb) {
   Plan pl;
-  const int64_t s = ceil_div(n, b);
+  (void)n;
   if (b == 1) {
-    pl.mat = (size_t)(m * n * 8);
-    if (n > K2_SMALL_CAP) pl.s2a = pl.s2b = (size_t)(m * kb * 8);
+    // whole-row exact select: only the k selected keys are stored (never
+    // the row's n keys), then K2 sorts them
+    pl.pool = (size_t)(m * k * 8);
+    if (k > K2_SMALL_CAP) pl.s2a = pl.s2b = (size_t)(m * k * 8);
     return pl;
   }
   pl.pool = (size_t)(m * b * kb * 8);
-  if (kb > 16) {
-    pl.mat = (size_t)(m * b * s * 8);
-    if (s > K2_SMALL_CAP) pl.s1a = pl.s1b = (size_t)(m * b * kb * 8);
-  }
   if (b * kb > K2_SMALL_CAP) pl.s2a = pl.s2b = (size_t)(m * k * 8);
+  return pl;
+}
+
+// Workspace of btk_stage1: the pool, plus the in-place per-bucket sort's
+// scratch when k_b > 16 exceeds one CTA's shared memory.
+Plan plan_stage1(int64_t m, int64_t b, int64_t kb) {
+  Plan pl;
+  pl.pool = (size_t)(m * b * kb * 8);
+  if (kb > 16 && kb > K2_SMALL_CAP) pl.s1a = pl.s1b = (size_t)(m * b * kb * 8);
   return pl;
 }
 
@@ -78,27 +85,23 @@ struct Carve {
   }
 };
 
-// Stage 1 into the bucket-major pool (m x b*kb comps).
-int stage1_pool(const Problem& p, const Plan& pl, Carve& cv, uint64_t* pool, cudaStream_t st) {
-  if (stage1_vec_supported(p)) return cuda_status(run_stage1_vec(p, pool, st));
+// Stage 1 into the bucket-major pool (m x b*kb comps).  `sorted`: every
+// bucket's k_b keys in canonical order (the stage1 API); Stage 2 only needs
+// the set.
+int stage1_pool(const Problem& p, const Plan& pl, Carve& cv, uint64_t* pool, cudaStream_t st, bool sorted) {
+  if (p.b > 1 && stage1_vec_supported(p)) return cuda_status(run_stage1_vec(p, pool, st));
   if (stage1_contig_supported(p)) return cuda_status(run_stage1_contig(p, pool, st));
   if (p.kb <= 16) return cuda_status(run_stage1_generic(p, pool, st));
-  uint64_t* mat = cv.take(pl.mat);
-  uint64_t* s1a = cv.take(pl.s1a);
-  uint64_t* s1b = cv.take(pl.s1b);
-  int rc = cuda_status(run_materialize(p, mat, st));
-  if (rc) return rc;
+  // k_b > 16: exact per-bucket radix select straight from the scores (no
+  // materialisation of the buckets), then, if asked, an in-place sort
+  int rc = cuda_status(run_select_raw(p.dtype, p.x, p.row_stride, p.m, p.n, p.b, p.layout, p.kb, pool,
+                                      p.geo, p.flag, st));
+  if (rc || !sorted) return rc;
   K2Args a{};
-  a.in = mat;
-  a.in_stride = ceil_div(p.n, p.b);
-  a.nseg = p.m * p.b;
-  a.L = a.in_stride;
-  a.kk = p.kb;
-  a.out_keys = pool;
-  a.out_stride = p.kb;
-  a.geo = p.geo;
-  a.scratch_a = s1a;
-  a.scratch_b = s1b;
+  a.in = pool; a.in_stride = p.kb; a.nseg = p.m * p.b; a.L = p.kb; a.kk = p.kb;
+  a.out_keys = pool; a.out_stride = p.kb; a.geo = p.geo;
+  a.scratch_a = cv.take(pl.s1a);
+  a.scratch_b = cv.take(pl.s1b);
   return cuda_status(run_k2(p.dtype, false, a, st));
 }
 
@@ -232,9 +235,8 @@ int btk_launch_count(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, int
     if (b > 1 && pool_chunked_ok(p)) return 3 + (k <= K2_SMALL_CAP ? 2 : 2);
   }
   auto k2n = [](int64_t L, int64_t kk) { return L <= K2_SMALL_CAP ? 1 : 2; };
-  if (b == 1) return 1 + k2n(n, k);
-  int c = (kb <= 16) ? 1 : 1 + k2n(ceil_div(n, b), kb);
-  return c + k2n(b * kb, k);
+  if (b == 1) return 1 + k2n(k, k);  // raw select + sort of the k selected
+  return 1 + k2n(b * kb, k);         // stage 1 (any form) + stage 2
 }
 
 int btk_approx_topk(const void* x, int64_t row_stride, int dtype, int64_t m, int64_t n, int64_t k,
@@ -287,24 +289,22 @@ int btk_approx_topk_flags(const void* x, int64_t row_stride, int dtype, int64_t 
     return cuda_status(run_pool_chunked(p, pool, cv.p, out_vals, out_idx, st));
   }
   if (b == 1) {
-    // single bucket: Stage 1 is already the exact canonical top-k (k_b == k)
-    uint64_t* mat = cv.take(pl.mat);
-    cv.take(pl.pool);
+    // single bucket: the exact canonical top-k of the row — radix select of
+    // the k largest straight from the scores, then K2 sorts those k
+    uint64_t* sel = cv.take(pl.pool);
     uint64_t* s2a = cv.take(pl.s2a);
     uint64_t* s2b = cv.take(pl.s2b);
-    rc = cuda_status(run_materialize(p, mat, st));
+    rc = cuda_status(run_select_raw(dtype, x, row_stride, m, n, 1, layout, k, sel, p.geo, flag, st));
     if (rc) return rc;
     K2Args a{};
-    a.in = mat; a.in_stride = n; a.nseg = m; a.L = n; a.kk = k;
+    a.in = sel; a.in_stride = k; a.nseg = m; a.L = k; a.kk = k;
     a.out_vals = out_vals; a.out_idx = out_idx; a.out_stride = k;
     a.geo = p.geo; a.scratch_a = s2a; a.scratch_b = s2b;
     return cuda_status(run_k2(dtype, true, a, st));
   }
   uint64_t* pool = cv.take(pl.pool);
-  Carve cv1 = cv;  // stage-1 scratch (mat, s1a, s1b) is dead before stage 2
-  rc = stage1_pool(p, pl, cv1, pool, st);
+  rc = stage1_pool(p, pl, cv, pool, st, false);
   if (rc) return rc;
-  cv.take(pl.mat); cv.take(pl.s1a); cv.take(pl.s1b);
   uint64_t* s2a = cv.take(pl.s2a);
   uint64_t* s2b = cv.take(pl.s2b);
   K2Args a{};
@@ -319,14 +319,7 @@ size_t btk_stage1_workspace_bytes(int64_t m, int64_t n, int64_t b, int64_t kb, i
   (void)layout;
   if (btk_stage1_validate(n, b, kb) != BTK_OK || m < 1) return 0;
   if (dtype == BTK_F64) return f64_stage1_workspace_bytes(m, n, b, kb);
-  Plan pl = plan_generic(m, n, std::max<int64_t>(1, std::min<int64_t>(n, b * kb)), b, kb);
-  pl.pool = (size_t)(m * b * kb * 8);
-  pl.s2a = pl.s2b = 0;
-  if (b == 1) {  // stage1 for b == 1 runs the bucket path too
-    pl.mat = (size_t)(m * n * 8);
-    pl.s1a = pl.s1b = (n > K2_SMALL_CAP && kb > 16) ? (size_t)(m * kb * 8) : 0;
-  }
-  return pl.total();
+  return plan_stage1(m, b, kb).total();
 }
 
 int btk_stage1(const void* x, int64_t row_stride, int dtype, int64_t m, int64_t n, int64_t b,
@@ -347,15 +340,10 @@ int btk_stage1(const void* x, int64_t row_stride, int dtype, int64_t m, int64_t 
   p.x = x; p.row_stride = row_stride; p.dtype = dtype;
   p.m = m; p.n = n; p.k = std::min<int64_t>(n, b * kb); p.b = b; p.kb = kb;
   p.layout = layout; p.geo = geo_for(dtype, n); p.flag = flag;
-  Plan pl = plan_generic(m, n, p.k, b, kb);
-  pl.pool = (size_t)(m * b * kb * 8);
-  if (b == 1) {
-    pl.mat = (size_t)(m * n * 8);
-    pl.s1a = pl.s1b = (n > K2_SMALL_CAP && kb > 16) ? (size_t)(m * kb * 8) : 0;
-  }
+  const Plan pl = plan_stage1(m, b, kb);
   Carve cv{static_cast<uint8_t*>(ws)};
   uint64_t* pool = cv.take(pl.pool);
-  rc = stage1_pool(p, pl, cv, pool, st);
+  rc = stage1_pool(p, pl, cv, pool, st, true);
   if (rc) return rc;
   const int64_t C = btk_stage1_count(n, b, kb, layout);
   return cuda_status(run_stage1_emit(p, pool, C, out_vals, out_idx, st));

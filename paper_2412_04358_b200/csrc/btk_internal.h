@@ -68,6 +68,11 @@ inline cudaError_t ensure_smem_attr(const void* fn, size_t bytes) {
 }
 
 cudaError_t run_k2(int dtype, bool decode, const K2Args& a, cudaStream_t st);
+// Exact top-kk composite keys of each of the nb buckets of m raw score
+// rows, unsorted (0 = empty), into out[m*nb][kk] — no materialisation of
+// the rows' n keys; K2 then sorts them.  nb = 1: whole rows.
+cudaError_t run_select_raw(int dtype, const void* x, int64_t row_stride, int64_t m, int64_t n, int64_t nb,
+                           int layout, int64_t kk, uint64_t* out, CompGeo g, uint32_t* flag, cudaStream_t st);
 cudaError_t run_decode(int dtype, const uint64_t* in, int64_t in_stride, int64_t nseg, int64_t kk,
                        void* out_vals, int64_t* out_idx, int64_t out_stride, CompGeo g,
                        cudaStream_t st);

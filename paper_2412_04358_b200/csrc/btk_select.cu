@@ -61,21 +61,39 @@ __global__ void __launch_bounds__(NT) k2_small(const uint64_t* __restrict__ in, 
 }
 
 // ---------------------------------------------------------------------------
-// MSD radix select + compaction for one long segment per CTA.
-template <int NT>
-__global__ void __launch_bounds__(NT) k2_select_compact(const uint64_t* __restrict__ in,
-                                                        int64_t in_stride, int64_t L, int64_t kk,
-                                                        uint64_t* __restrict__ out,
-                                                        int64_t out_stride, int nbits,
-                                                        const int* mask, int64_t mask_stride) {
+// MSD radix select + compaction for one long segment per CTA.  The keys come
+// from a SOURCE: a segment of materialised composite keys, or a raw score
+// row whose composite keys are formed on the fly (element e -> comp(vkey,
+// e, negzero)), so an exact top-k over whole rows never materialises m*n
+// keys (it writes only the kk selected).
+struct CompSource {
+  const uint64_t* p;
+  __device__ __forceinline__ uint64_t key(int64_t i, uint32_t&) const { return p[i]; }
+};
+template <int DT>
+struct RawSource {  // slot i of a bucket = element start + i*step of its row
+  const void* row;
+  int64_t start, step;
+  CompGeo g;
+  __device__ __forceinline__ uint64_t key(int64_t i, uint32_t& bad) const {
+    const int64_t e = start + i * step;
+    const uint32_t bits = load_bits<DT>(row, e);
+    bad |= nonfinite<DT>(bits) ? 1u : 0u;
+    return make_comp(vkey<DT>(bits), (uint32_t)e, is_negzero<DT>(bits), g);
+  }
+};
+
+template <int NT, class Src>
+__device__ __forceinline__ void select_compact(const Src& src, int64_t L, int64_t kk, uint64_t* __restrict__ dst,
+                                               int nbits, uint32_t& bad) {
   __shared__ uint32_t hist[RADIX];
   __shared__ int s_bin;
   __shared__ uint32_t s_above;
   __shared__ uint32_t s_cnt;
-  const int64_t seg = blockIdx.x;
-  if (mask && mask[seg * mask_stride] >= 0) return;
-  const uint64_t* src = in + seg * in_stride;
-  uint64_t* dst = out + seg * out_stride;
+  if (L <= kk) {  // the whole segment is selected; empty slots (0) sort last
+    for (int64_t p = threadIdx.x; p < kk; p += NT) dst[p] = p < L ? src.key(p, bad) : 0ull;
+    return;
+  }
   uint64_t prefix = 0;
   uint32_t need = (uint32_t)kk;
   int shift = nbits;
@@ -87,7 +105,7 @@ __global__ void __launch_bounds__(NT) k2_select_compact(const uint64_t* __restri
     __syncthreads();
     const int hs = shift + w;
     for (int64_t p = threadIdx.x; p < L; p += NT) {
-      uint64_t key = src[p];
+      uint64_t key = src.key(p, bad);
       uint64_t hi = (hs >= 64) ? 0ull : (key >> hs);
       if (hi == prefix) atomicAdd(&hist[(uint32_t)(key >> shift) & ((1u << w) - 1u)], 1u);
     }
@@ -111,7 +129,7 @@ __global__ void __launch_bounds__(NT) k2_select_compact(const uint64_t* __restri
   const int lane = threadIdx.x & 31;
   for (int64_t p0 = 0; p0 < L; p0 += NT) {
     int64_t p = p0 + threadIdx.x;
-    uint64_t key = (p < L) ? src[p] : 0ull;
+    uint64_t key = (p < L) ? src.key(p, bad) : 0ull;
     bool take = (p < L) && (early ? (key >= thr) : (key > thr));
     uint32_t ball = __ballot_sync(0xFFFFFFFFu, take);
     uint32_t base = 0;
@@ -121,6 +139,41 @@ __global__ void __launch_bounds__(NT) k2_select_compact(const uint64_t* __restri
   }
   __syncthreads();
   for (int64_t p = s_cnt + threadIdx.x; p < kk; p += NT) dst[p] = thr;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k2_select_compact(const uint64_t* __restrict__ in,
+                                                        int64_t in_stride, int64_t L, int64_t kk,
+                                                        uint64_t* __restrict__ out,
+                                                        int64_t out_stride, int nbits,
+                                                        const int* mask, int64_t mask_stride) {
+  const int64_t seg = blockIdx.x;
+  if (mask && mask[seg * mask_stride] >= 0) return;
+  uint32_t bad = 0;
+  select_compact<NT>(CompSource{in + seg * in_stride}, L, kk, out + seg * out_stride, nbits, bad);
+}
+
+// Exact top-kk composite keys of every bucket of raw score rows, unsorted
+// (0 = empty slot): one CTA per (row, bucket), buckets laid out as in the
+// reference (interleaved j + b*t / contiguous slices, core.py:124-147).
+template <int DT, int NT>
+__global__ void __launch_bounds__(NT) k2_select_raw(const void* __restrict__ x, int64_t row_stride, int64_t n,
+                                                    int64_t nb, int layout, int64_t kk,
+                                                    uint64_t* __restrict__ out, CompGeo g, uint32_t* flag) {
+  const int64_t seg = blockIdx.x, row = seg / nb, j = seg - row * nb;
+  int64_t start, size, step;
+  if (layout == 0) {
+    const int64_t q = n / nb, r = n % nb;
+    start = j; size = q + (j < r ? 1 : 0); step = nb;
+  } else {
+    start = (j * n + nb - 1) / nb;
+    size = ((j + 1) * n + nb - 1) / nb - start;
+    step = 1;
+  }
+  uint32_t bad = 0;
+  const RawSource<DT> src{static_cast<const uint8_t*>(x) + row * row_stride * (VT<DT>::W / 8), start, step, g};
+  select_compact<NT>(src, size, kk, out + seg * kk, g.nbits, bad);
+  if (__syncthreads_or(bad) && threadIdx.x == 0 && flag) atomicOr(flag, 1u);
 }
 
 // ---------------------------------------------------------------------------
@@ -255,6 +308,32 @@ static cudaError_t run_k2_t(const K2Args& a, cudaStream_t st) {
   k2_global_lsd<DT, 512, 8, DECODE><<<(unsigned)a.nseg, 512, 0, st>>>(
       a.scratch_a, a.scratch_b, sa, sb, a.kk, a.out_keys, a.out_vals, a.out_idx, a.out_stride, a.geo,
       a.mask, a.mask_stride);
+  return cudaGetLastError();
+}
+
+template <int DT, int NT>
+static void launch_select_raw(const void* x, int64_t row_stride, int64_t m, int64_t n, int64_t nb, int layout,
+                              int64_t kk, uint64_t* out, CompGeo g, uint32_t* flag, cudaStream_t st) {
+  k2_select_raw<DT, NT><<<(unsigned)(m * nb), NT, 0, st>>>(x, row_stride, n, nb, layout, kk, out, g, flag);
+}
+
+template <int DT>
+static void select_raw_dt(const void* x, int64_t row_stride, int64_t m, int64_t n, int64_t nb, int layout,
+                          int64_t kk, uint64_t* out, CompGeo g, uint32_t* flag, cudaStream_t st) {
+  if (n / nb >= 16384) launch_select_raw<DT, 1024>(x, row_stride, m, n, nb, layout, kk, out, g, flag, st);
+  else launch_select_raw<DT, 256>(x, row_stride, m, n, nb, layout, kk, out, g, flag, st);
+}
+
+cudaError_t run_select_raw(int dtype, const void* x, int64_t row_stride, int64_t m, int64_t n, int64_t nb,
+                           int layout, int64_t kk, uint64_t* out, CompGeo g, uint32_t* flag, cudaStream_t st) {
+  if (m == 0) return cudaSuccess;
+  if (m * nb > 0x7FFFFFFFll) return cudaErrorInvalidValue;
+  switch (dtype) {
+    case F32: select_raw_dt<F32>(x, row_stride, m, n, nb, layout, kk, out, g, flag, st); break;
+    case BF16: select_raw_dt<BF16>(x, row_stride, m, n, nb, layout, kk, out, g, flag, st); break;
+    case F16: select_raw_dt<F16>(x, row_stride, m, n, nb, layout, kk, out, g, flag, st); break;
+    default: return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 

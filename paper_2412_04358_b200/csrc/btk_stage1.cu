@@ -166,7 +166,14 @@ __global__ void __launch_bounds__(256) s1_contig(Problem p, uint64_t* __restrict
             if (v0 + G * u < nv) sc.row(w[u], (int)(v0 + G * u));
         }
         bad |= sc.nonfinite() ? 1u : 0u;
-        sc.each_comp(0, V, start / V, p.geo, [&](int64_t, int, uint64_t c) { fz::comp_push<KB>(best, c); });
+        // each_comp indexes code*V + slot from the slice start; the slice may
+        // start at any element (row bases need not be 16-byte aligned), so
+        // shift the index field by `start` (comp - 2*start: the field holds
+        // IMAX - idx and never borrows into the value bits)
+        const uint64_t shift_start = (uint64_t)start << 1;
+        sc.each_comp(0, V, 0, p.geo, [&](int64_t, int, uint64_t c) {
+          if (c) fz::comp_push<KB>(best, c - shift_start);
+        });
       } else {
         fz::Queue<KB> q;
         q.init();

@@ -72,3 +72,32 @@ def test_contig_cfg3_shape_full_rows():
     rows = [0, 17, 127]
     wv, wi = O.approx_topk(x[rows].float().cpu().numpy(), k, b, kb, "contiguous")
     np.testing.assert_array_equal(r.indices[rows].cpu().numpy(), wi)
+
+
+def test_exact_and_large_kb_select_without_materialising():
+    """exact_topk_oracle (b = 1) and k_b > 16 stage 1 select straight from
+    the scores: the workspace is O(m*k), not O(m*n) (a 8192 x 2^20 exact
+    top-65536 needs 12.9 GB instead of 68.7 GB), and the results are the
+    oracle's (reference exact.py:162-173, approx.py:142-164)."""
+    lib = _lib.load()
+    assert lib.btk_exact_workspace_bytes(8192, 1 << 20, 65536, _lib.BTK_BF16) < 8192 * (1 << 20) * 8 // 5
+    assert lib.btk_exact_workspace_bytes(128, 65536, 64, _lib.BTK_F32) <= 128 * 64 * 8 + 512
+    rng = np.random.default_rng(31)
+    x32 = torch.from_numpy(rng.standard_normal((3, 1 << 20), dtype=np.float32)).to(torch.bfloat16).float().numpy()
+    x32[1, ::3] = 0.25  # heavy ties at the boundary
+    x = to_dtype(x32, "bf16").cuda()
+    for k in (37, 20000):
+        e = btk.exact_topk_oracle(x, k)
+        wv, wi = O.exact_topk(x32, k)
+        np.testing.assert_array_equal(e.indices.cpu().numpy(), wi)
+    for (n, b, kb, asg) in [(50000, 100, 300, "interleaved"), (50000, 100, 300, "contiguous"), (70000, 7, 17, "interleaved")]:
+        xs = rng.standard_normal((2, n), dtype=np.float32)
+        xs[0, ::4] = -0.0
+        A = btk.Assignment.from_string(asg)
+        k = min(b * kb, 1000)
+        r = btk.approx_topk(torch.from_numpy(xs).cuda(), k, btk.BucketScheme(b, kb, A))
+        wv, wi = O.approx_topk(xs, k, b, kb, asg)
+        np.testing.assert_array_equal(r.indices.cpu().numpy(), wi)
+        s = btk.stage1(torch.from_numpy(xs).cuda(), btk.BucketScheme(b, kb, A))
+        sv, si, _ = O.stage1(O.as_matrix(xs), b, kb, asg)
+        np.testing.assert_array_equal(s.indices.cpu().numpy(), si)
