@@ -112,8 +112,6 @@ bool pool_chunked_ok(const Problem& p);
 size_t pool_chunked_bytes(const Problem& p);  // hist + tab + chunk buffer
 cudaError_t run_pool_chunked(const Problem& p, uint64_t* pool, void* ws, void* out_vals,
                              int64_t* out_idx, cudaStream_t st);
-// All of a row's elements as comps, bucket-major (m*b segments of s slots).
-cudaError_t run_materialize(const Problem& p, uint64_t* mat, cudaStream_t st);
 // pool (m x b*kb) -> compact (m x C) values/indices in bucket order.
 cudaError_t run_stage1_emit(const Problem& p, const uint64_t* pool, int64_t C, void* out_vals,
                             int64_t* out_idx, cudaStream_t st);

@@ -69,28 +69,6 @@ __global__ void __launch_bounds__(256) s1_generic(Problem p, uint64_t* __restric
 }
 
 template <int DT>
-__global__ void s1_materialize(Problem p, uint64_t* __restrict__ mat) {
-  const int64_t s = (p.n + p.b - 1) / p.b;
-  const int64_t total = p.m * p.b * s;
-  bool bad = false;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t slot = t % s;
-    const int64_t rb = t / s;
-    const int64_t j = rb % p.b, row = rb / p.b;
-    int64_t start, size, step;
-    bucket_span(p, j, start, size, step);
-    uint64_t c = 0ull;
-    if (slot < size) {
-      const void* xr = static_cast<const uint8_t*>(p.x) + row * p.row_stride * (VT<DT>::W / 8);
-      c = elem_comp<DT>(p, xr, start + slot * step, bad);
-    }
-    mat[t] = c;
-  }
-  if (__syncthreads_or(bad) && threadIdx.x == 0 && p.flag) atomicOr(p.flag, 1u);
-}
-
-template <int DT>
 __global__ void s1_emit(Problem p, const uint64_t* __restrict__ pool, int64_t C,
                         void* __restrict__ out_vals, int64_t* __restrict__ out_idx) {
   const int64_t total = p.m * p.b * p.kb;
@@ -273,18 +251,6 @@ cudaError_t run_stage1_generic(const Problem& p, uint64_t* pool, cudaStream_t st
 
 static unsigned grid_for(int64_t total) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 64));
-}
-
-cudaError_t run_materialize(const Problem& p, uint64_t* mat, cudaStream_t st) {
-  const int64_t s = (p.n + p.b - 1) / p.b;
-  const unsigned g = grid_for(p.m * p.b * s);
-  switch (p.dtype) {
-    case F32: s1_materialize<F32><<<g, 256, 0, st>>>(p, mat); break;
-    case BF16: s1_materialize<BF16><<<g, 256, 0, st>>>(p, mat); break;
-    case F16: s1_materialize<F16><<<g, 256, 0, st>>>(p, mat); break;
-    default: return cudaErrorInvalidValue;
-  }
-  return cudaGetLastError();
 }
 
 cudaError_t run_stage1_emit(const Problem& p, const uint64_t* pool, int64_t C, void* out_vals,
