@@ -46,6 +46,7 @@
 #include <cstdlib>
 
 #include "btk_internal.h"
+#include "btk_lsd.cuh"
 #include "btk_rank.cuh"
 #include "btk_sort.cuh"
 
@@ -873,6 +874,7 @@ struct WideArgs {
   uint32_t* flag;
   int trace;
   int early;  // read the input before the predecessor completes (BTK_INPUT_READY)
+  int lsd_lowbit;  // > 0: large pool, stable LSD Stage 2 from this bit (btk_lsd.cuh)
 };
 
 template <int DT, int KB, int NT, int U, int ITEMS>
@@ -919,12 +921,34 @@ __global__ void __launch_bounds__(NT, 1) fused_wide(WideArgs a) {
     for (int e = 0; e < V; ++e) {
       const int64_t col = g * V + e;
 #pragma unroll
-      for (int z = 0; z < KB; ++z)
-        if (z < a.kb) pool[col * a.kb + z] = comp_of<DT>(q[e].v[z], q[e].t[z], col, b, a.geo);
+      for (int z = 0; z < KB; ++z) {
+        if (z < a.kb) {
+          const int p = (int)(col * a.kb + z);  // bucket-id order
+          pool[a.lsd_lowbit ? lsd::pad32(p) : p] = comp_of<DT>(q[e].v[z], q[e].t[z], col, b, a.geo);
+        }
+      }
     }
   }
   if (tr) g_trace[blockIdx.x][2] = g_trace[blockIdx.x][3] = gtime();
   if (__syncthreads_or(nonfinite_hit<DT>(bad)) && tid == 0 && a.flag) atomicOr(a.flag, 1u);
+  if constexpr (ITEMS == 32) {
+    if (a.lsd_lowbit) {
+      // large pool: stable in-place LSD (5-bit digits, per-thread counters)
+      // over the bits above the bucket id — the pool is already in bucket-id
+      // order — instead of the atomic-bucketing rank engine
+      __shared__ uint32_t lws[NT / 32][16];
+      __shared__ uint32_t ltot[32], ldex[32];
+      __shared__ unsigned long long lvary;
+      lsd::sort_desc_inplace<NT, 32, 5>(pool, (int)a.P, a.lsd_lowbit,
+                                        reinterpret_cast<uint32_t*>(smem + a.aux_off), lws, ltot, ldex, &lvary);
+      if (tr) g_trace[blockIdx.x][5] = gtime();
+      pdl_wait_writes(a.early != 0);
+      for (int64_t q = tid; q < a.k; q += NT)
+        emit_comp<DT>(pool[lsd::pad32((int)q)], row * a.k + q, a.geo, a.out_vals, a.out_idx);
+      if (tr) g_trace[blockIdx.x][4] = gtime();
+      return;
+    }
+  }
   stage2_emit<DT, NT, ITEMS>(pool, smem + a.aux_off, a.P, a.k, a.lognb, row, a.geo, a.out_vals,
                             a.out_idx, a.trace != 0, a.early != 0);
   if (tr) g_trace[blockIdx.x][4] = gtime();
@@ -1125,6 +1149,19 @@ inline bool plan_wide(const Problem& p, Plan& pl) {
   a.trace = env_int("BTK_TRACE", 0);
   a.early = (p.flags & 1u) && pdl_enabled() ? 1 : 0;
   pl.smem = stage2_bytes(P, p.k, WIDE_NT);
+  a.lsd_lowbit = 0;
+  // opt-in (BTK_WIDE_LSD=1): measured slower than the rank engine at cfg2
+  // (61.6 vs 43 us: fp32 owner keys vary in ~35 bits above the bucket id,
+  // 7 five-bit passes)
+  if (a.sort_items == 32 && env_int("BTK_WIDE_LSD", 0)) {
+    // the pool is in bucket-id order: for b a power of two the low log2(b)
+    // bits of the index field (~j) are already sorted
+    int lb = 0;
+    while ((int64_t(1) << lb) < p.b) ++lb;
+    a.lsd_lowbit = ((p.b & (p.b - 1)) == 0) ? 1 + lb : 1;
+    a.aux_off = a16((size_t)lsd::pad32((int)P) * 8);
+    pl.smem = a.aux_off + (size_t)16 * WIDE_NT * 4;  // pool (padded) + 16 counter words per thread
+  }
   pl.kind = WIDE;
   pl.nt = WIDE_NT;
   return pl.smem <= SMEM_LIMIT;

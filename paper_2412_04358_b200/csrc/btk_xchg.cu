@@ -136,80 +136,13 @@ __device__ __forceinline__ uint64_t from_rec(KT r, uint32_t j, const XArgs& a) {
   }
 }
 
-// Block-wide digit scan over per-thread counters kept in shared memory:
-// cnt[q * NT + tid] packs the thread's counts of digits 2q (low 16 bits)
-// and 2q+1 (high 16 bits), q < 8.  On return cnt holds the thread's
-// exclusive base per digit (within the digit, in thread order), tot[d] the
-// block total of digit d and dex[d] the digit-concatenated exclusive base.
+// Per-thread digit counters and the block digit scan: btk_lsd.cuh (4-bit
+// digits here: 8 counter words per thread).
+using lsd::count_digit;
+using lsd::digit_base;
 template <int NT>
 __device__ __forceinline__ void digit_scan(uint32_t* cnt, uint32_t (*ws)[8], uint32_t* tot, uint32_t* dex) {
-  constexpr int NW = NT / 32;
-  constexpr int GW = NW / 4;  // warps per group in the cross-warp scan
-  static_assert(NW % 4 == 0, "NT multiple of 128");
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint32_t own[8], w[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) w[q] = own[q] = cnt[q * NT + tid];
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, w[q], o);
-      if (lane >= o) w[q] += t;
-    }
-  }
-  if (lane == 31) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) ws[warp][q] = w[q];
-  }
-  __syncthreads();
-  if (warp == 0) {  // lane = word q (lane & 7) x warp group g (lane >> 3)
-    const int q = lane & 7, g = lane >> 3;
-    uint32_t v[GW], s4 = 0;
-#pragma unroll
-    for (int i = 0; i < GW; ++i) { v[i] = ws[g * GW + i][q]; s4 += v[i]; }
-    uint32_t x = s4;
-    uint32_t t = __shfl_up_sync(0xFFFFFFFFu, x, 8);
-    if (g >= 1) x += t;
-    t = __shfl_up_sync(0xFFFFFFFFu, x, 16);
-    if (g >= 2) x += t;
-    uint32_t run = x - s4;
-#pragma unroll
-    for (int i = 0; i < GW; ++i) { ws[g * GW + i][q] = run; run += v[i]; }
-    const uint32_t all = __shfl_sync(0xFFFFFFFFu, x, 24 + q);  // word q total (group 3 inclusive)
-    if (g == 0) {
-      const uint32_t lo = all & 0xFFFFu, hi = all >> 16, pair = lo + hi;
-      uint32_t e = pair;
-#pragma unroll
-      for (int o = 1; o < 8; o <<= 1) {
-        const uint32_t u = __shfl_up_sync(0x000000FFu, e, o);
-        if (q >= o) e += u;
-      }
-      e -= pair;
-      tot[2 * q] = lo;
-      tot[2 * q + 1] = hi;
-      dex[2 * q] = e;
-      dex[2 * q + 1] = e + lo;
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < 8; ++q) cnt[q * NT + tid] = w[q] - own[q] + ws[warp][q];
-}
-
-// count one item of digit d (< 16) in the thread's smem counters; returns
-// the number of earlier items of this thread with that digit
-template <int NT>
-__device__ __forceinline__ uint32_t count_digit(uint32_t* cnt, uint32_t d) {
-  uint32_t* c = cnt + (d >> 1) * NT + threadIdx.x;
-  const uint32_t sh = (d & 1u) << 4;
-  const uint32_t v = *c;
-  *c = v + (1u << sh);
-  return (v >> sh) & 0xFFFFu;
-}
-template <int NT>
-__device__ __forceinline__ uint32_t digit_base(const uint32_t* cnt, uint32_t d) {
-  return (cnt[(d >> 1) * NT + threadIdx.x] >> ((d & 1u) << 4)) & 0xFFFFu;
+  lsd::digit_scan<NT, 8>(cnt, ws, tot, dex);
 }
 
 // Shared-memory carve-up (bytes), identical on host and device.
