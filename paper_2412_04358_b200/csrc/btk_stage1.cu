@@ -102,15 +102,18 @@ __global__ void s1_emit(Problem p, const uint64_t* __restrict__ pool, int64_t C,
 // in increasing index order = first maximum); the 32 queues then merge by
 // k_b rounds of a warp max over composite keys (unique, canonical order).
 // Slices that do not start/end on a 16-byte boundary take scalar loads.
-template <int DT, int KB>
-__global__ void __launch_bounds__(256) s1_contig(Problem p, uint64_t* __restrict__ pool, int G) {
+template <int DT, int KB, int U>
+__global__ void __launch_bounds__(256, (U <= 4 ? 4 : 2)) s1_contig(Problem p, uint64_t* __restrict__ pool, int G) {
   constexpr int V = 16 / (VT<DT>::W / 8);
   constexpr int ESZ = VT<DT>::W / 8;
-  constexpr int U = 8;  // vectors in flight per lane
   const int lane = threadIdx.x & 31, gl = lane % G, per_warp = 32 / G;
   const int64_t P = p.b * p.kb;
   const int64_t tasks = p.m * p.b;
   uint32_t bad = 0;
+  // uniform buckets (b | n) and < 2^32 tasks: 32-bit index math, no 64-bit
+  // divisions per bucket (they cost more than a bucket's loads)
+  const bool uni = (p.n % p.b) == 0 && tasks < (int64_t(1) << 32) && p.b < (int64_t(1) << 31);
+  const uint32_t b32 = (uint32_t)p.b, bsz = (uint32_t)(p.n / p.b);
   for (int64_t t0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * per_warp; t0 < tasks;
        t0 += (int64_t)gridDim.x * 8 * per_warp) {
     const int64_t task = t0 + lane / G;  // this lane group's (row, bucket)
@@ -119,10 +122,18 @@ __global__ void __launch_bounds__(256) s1_contig(Problem p, uint64_t* __restrict
     for (int z = 0; z < KB; ++z) best[z] = 0ull;
     int64_t row = 0, j = 0;
     if (task < tasks) {
-      row = task / p.b;
-      j = task - row * p.b;
       int64_t start, size, step;
-      bucket_span(p, j, start, size, step);
+      if (uni) {
+        const uint32_t r32 = (uint32_t)task / b32;
+        row = r32;
+        j = (uint32_t)task - r32 * b32;
+        start = (int64_t)((uint32_t)j * bsz);
+        size = bsz;
+      } else {
+        row = task / p.b;
+        j = task - row * p.b;
+        bucket_span(p, j, start, size, step);
+      }
       const uint8_t* xr = static_cast<const uint8_t*>(p.x) + row * p.row_stride * ESZ;
       const bool vec = ((reinterpret_cast<uintptr_t>(xr) + start * ESZ) & 15) == 0 && (size % V) == 0 &&
                        size / V < 0xFFFF;
@@ -190,14 +201,18 @@ __global__ void __launch_bounds__(256) s1_contig(Problem p, uint64_t* __restrict
 
 template <int DT, int KB>
 static cudaError_t launch_contig(const Problem& p, uint64_t* pool, cudaStream_t st) {
-  // lanes per bucket: enough that each lane streams >= 16 vectors of it
+  // lanes per bucket: each lane streams >= 64 vectors of its bucket (the
+  // per-bucket merge is amortised; measured at cfg3-contiguous: 16 -> 4.8,
+  // 32 -> 4.9, 64 -> 5.1, 128 -> 4.6 TB/s)
   const int V = 16 / (VT<DT>::W / 8);
   const int64_t nv = (p.n / p.b) / V;
+  const int vpl = fz::env_int("BTK_CONTIG_VPL", 64);  // min vectors per lane
   int G = 1;
-  while (G < 32 && nv / (2 * G) >= 16) G *= 2;
+  while (G < 32 && nv / (2 * G) >= vpl) G *= 2;
   const int64_t blocks = (p.m * p.b + 8 * (32 / G) - 1) / (8 * (32 / G));
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 16));
-  s1_contig<DT, KB><<<grid, 256, 0, st>>>(p, pool, G);
+  if (fz::env_int("BTK_CONTIG_U", 4) == 8) s1_contig<DT, KB, 8><<<grid, 256, 0, st>>>(p, pool, G);
+  else s1_contig<DT, KB, 4><<<grid, 256, 0, st>>>(p, pool, G);
   return cudaGetLastError();
 }
 
