@@ -36,10 +36,9 @@
 //   5. emit       the owner decodes its first min(count, k - start) keys
 //                 into (value bits, int64 index) at its output offset.
 //
-// Fallback rows (rowmask = -1: partition overflow, or a 16-bit owner range
-// too wide for 32-bit sort keys) write their Stage-1 survivors in the
-// generic pool layout, and the row-masked K2 (btk_select.cu) launched
-// right after finishes them; other rows make it exit at once.
+// Fallback rows (partition overflow, or a 16-bit owner range too wide for
+// 32-bit sort keys) go to a device-side list; xc_fallback recomputes them
+// with per-CTA scratch (its CTAs exit at once when the list is empty).
 //
 // Keys: for 16-bit dtypes a candidate is a 32-bit record
 // (vkey16 << 16 | (0x7FFF - t) << 1 | negzero) with j implied by its
@@ -47,6 +46,7 @@
 // owner's range floor aligned to the value field; fp32 uses the 64-bit
 // composite key (btk_common.cuh) throughout.
 #include "btk_fused_impl.cuh"
+#include "btk_k2dev.cuh"
 
 namespace btk {
 namespace xc {
@@ -102,8 +102,8 @@ struct XArgs {
   void* out_vals;
   int64_t* out_idx;
   uint32_t* flag;
-  int* rowmask;    // per row: 0 handled here, -1 generic fallback
-  uint64_t* pool;  // fallback rows: m x (b*k_b) comps, bucket-major (s1_vec layout)
+  int* fb_count;   // rows whose partition overflowed (zeroed before the launch) ...
+  int* fb_list;    // ... and their ids, finished by xc_fallback
   int trace;       // development timeline (BTK_XC_TRACE=1): globaltimer per CTA and phase
   int early;       // read the input before the predecessor completes (BTK_INPUT_READY)
 };
@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(NT, 2) fused_xchg(XArgs a) {
   __syncthreads();
   if (tid == 0) {  // fallback verdict, output offset and receive count (one thread)
     uint64_t sum = 0, st = 0;
-    int why = 0;  // fallback reasons (rowmask = -1 - why): 1 overflow, 2 key range, 4 short
+    int why = 0;  // fallback reasons: 1 owner overflow, 2 key range, 4 threshold kept < k
     for (int d = 0; d < C; ++d) {
       if ((uint32_t)d < rank) st += tot[d];
       sum += tot[d];
@@ -397,14 +397,10 @@ __global__ void __launch_bounds__(NT, 2) fused_xchg(XArgs a) {
   const int R = (int)tot[rank];
   pdl_wait_writes(a.early != 0);  // first global writes below
   if (s_why) {  // identical verdict in every CTA (same splitters, same totals)
-    if (rank == 0 && tid == 0) a.rowmask[row] = -1 - s_why;
-    uint64_t* dst = a.pool + row * a.b * KB + col0 * KB;
-    for (int p = tid; p < a.ncand; p += NT)
-      dst[p] = from_rec<KT>(cand[padk<KT>(p)], (uint32_t)(col0 + p / KB), a);
+    if (rank == 0 && tid == 0) a.fb_list[atomicAdd(a.fb_count, 1)] = (int)row;
     cluster_sync_all();  // peers may still read this CTA's send counts
     return;
   }
-  if (rank == 0 && tid == 0) a.rowmask[row] = 0;
   {
     const uint32_t recv_s = smem_u32(recv);
 #pragma unroll
@@ -485,6 +481,74 @@ __global__ void __launch_bounds__(NT, 2) fused_xchg(XArgs a) {
     emit_comp<DT>(c, row * a.k + start + q, geo, a.out_vals, a.out_idx);
   }
   mark(a, 7);
+}
+
+// ================================================================ fallback
+// Rows whose value partition overflowed (massive ties, or 16-bit owner
+// ranges too wide for 32-bit keys), one CTA per row from a persistent grid
+// over the device-side list: Stage 1 of the row again (same scanners) into
+// the CTA's scratch slot, the MSD radix select of the k largest, a stable
+// LSD through the slot, emit.  Scratch is per CTA, not per row: the
+// workspace no longer grows with m (cfg5: 0.23 GB instead of 12.9 GB).
+constexpr int FB_CTAS = 148;
+constexpr int FB_NT = 512;
+
+template <int DT, int KB>
+__global__ void __launch_bounds__(FB_NT) xc_fallback(XArgs a, uint64_t* __restrict__ slots, int64_t slot_stride) {
+  constexpr int V = Vec<DT>::V;
+  constexpr int ESZ = VT<DT>::W / 8;
+  constexpr int U = 8;
+  const int cnt = *a.fb_count;
+  if ((int)blockIdx.x >= cnt) return;
+  const int tid = threadIdx.x;
+  const int64_t P = a.b * KB;
+  uint64_t* pool = slots + (int64_t)blockIdx.x * slot_stride;  // P keys
+  uint64_t* sel = pool + P;                                     // k keys
+  const int gv = (int)(a.b / V);
+  for (int i = blockIdx.x; i < cnt; i += gridDim.x) {
+    const int64_t row = a.fb_list[i];
+    const uint8_t* rowp = static_cast<const uint8_t*>(a.x) + row * a.row_stride * ESZ;
+    const int64_t vstride = a.b * ESZ;
+    for (int g = tid; g < gv; g += FB_NT) {
+      Scanner<DT, KB> sc;
+      sc.init();
+      const uint8_t* colp = rowp + (int64_t)g * V * ESZ;
+      for (int t0 = 0; t0 < a.s; t0 += U) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          v[u] = (t0 + u < a.s) ? ldg_stream(colp + (int64_t)(t0 + u) * vstride) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (t0 + u < a.s) sc.row(v[u], t0 + u);
+      }
+      sc.each_comp(g, a.b, 0, a.geo, [&](int64_t col, int z, uint64_t c) { pool[col * KB + z] = c; });
+    }
+    __syncthreads();
+    uint32_t bad = 0;  // non-finite input was flagged by the cluster kernel
+    select_compact<FB_NT>(CompSource{pool}, P, a.k, sel, a.geo.nbits, bad);
+    __syncthreads();
+    const uint64_t* res = global_lsd<FB_NT, 8>(sel, pool, a.k, a.geo.nbits);
+    for (int64_t q = tid; q < a.k; q += FB_NT) emit<DT>(res[q], row * a.k + q, a.geo, a.out_vals, a.out_idx);
+    __syncthreads();
+  }
+}
+
+template <int DT>
+cudaError_t launch_fallback(const XArgs& a, int64_t kb, uint64_t* slots, int64_t slot_stride, cudaStream_t st) {
+  const unsigned grid = (unsigned)std::min<int64_t>(a.m, FB_CTAS);
+  switch (kb) {
+    case 1: xc_fallback<DT, 1><<<grid, FB_NT, 0, st>>>(a, slots, slot_stride); break;
+    case 2: xc_fallback<DT, 2><<<grid, FB_NT, 0, st>>>(a, slots, slot_stride); break;
+    case 4: xc_fallback<DT, 4><<<grid, FB_NT, 0, st>>>(a, slots, slot_stride); break;
+    default:
+      if constexpr (DT == F32) {
+        xc_fallback<DT, 8><<<grid, FB_NT, 0, st>>>(a, slots, slot_stride);
+        break;
+      }
+      return cudaErrorNotSupported;
+  }
+  return cudaGetLastError();
 }
 
 // ================================================================ host side
@@ -610,46 +674,44 @@ bool xchg_supported(const Problem& p) {
 static size_t al256(size_t v) { return (v + 255) & ~(size_t)255; }
 
 size_t xchg_workspace_bytes(const Problem& p) {
-  // row mask + the generic fallback's pool (+ its long-segment scratch)
+  // fallback-row counter + list, and one scratch slot (pool + k keys) per
+  // fallback CTA
   const int64_t P = p.b * p.kb;
-  size_t v = al256((size_t)p.m * 4) + al256((size_t)p.m * P * 8);
-  if (P > K2_SMALL_CAP) v += al256((size_t)p.m * p.k * 8);
-  return v;
+  const int64_t ctas = std::min<int64_t>(p.m, xc::FB_CTAS);
+  return al256(4) + al256((size_t)p.m * 4) + al256((size_t)ctas * (P + p.k) * 8);
 }
 
 cudaError_t run_xchg(const Problem& p, void* ws, void* out_vals, int64_t* out_idx, cudaStream_t st) {
   xc::XArgs a{};
   if (!xc::plan(p, a)) return cudaErrorNotSupported;
   uint8_t* w = static_cast<uint8_t*>(ws);
-  int* rowmask = reinterpret_cast<int*>(w);
+  int* count = reinterpret_cast<int*>(w);
+  w += al256(4);
+  int* list = reinterpret_cast<int*>(w);
   w += al256((size_t)p.m * 4);
-  uint64_t* pool = reinterpret_cast<uint64_t*>(w);
+  uint64_t* slots = reinterpret_cast<uint64_t*>(w);
   const int64_t P = p.b * p.kb;
-  w += al256((size_t)p.m * P * 8);
-  uint64_t* scratch = P > K2_SMALL_CAP ? reinterpret_cast<uint64_t*>(w) : nullptr;
   a.out_vals = out_vals;
   a.out_idx = out_idx;
-  a.rowmask = rowmask;
-  a.pool = pool;
+  a.fb_count = count;
+  a.fb_list = list;
   a.trace = fz::env_int("BTK_XC_TRACE", 0);
   a.early = (p.flags & 1u) && fz::pdl_enabled() ? 1 : 0;
-  cudaError_t e = cudaErrorInvalidValue;
+  cudaError_t e = cudaMemsetAsync(count, 0, sizeof(int), st);
+  if (e != cudaSuccess) return e;
   switch (p.dtype) {
     case F32: e = xc::launch_dt<F32>(a, p.kb, st); break;
     case BF16: e = xc::launch_dt<BF16>(a, p.kb, st); break;
     case F16: e = xc::launch_dt<F16>(a, p.kb, st); break;
+    default: e = cudaErrorInvalidValue;
   }
   if (e != cudaSuccess) return e;
-  // rows the partition could not place (rowmask -1): K2 over their pools
-  K2Args k2{};
-  k2.in = pool; k2.in_stride = P; k2.nseg = p.m; k2.L = P; k2.kk = p.k;
-  k2.out_vals = out_vals; k2.out_idx = out_idx; k2.out_stride = p.k;
-  k2.geo = p.geo;
-  k2.scratch_a = scratch; k2.scratch_b = pool;
-  k2.scratch_a_stride = p.k; k2.scratch_b_stride = P;
-  k2.mask = rowmask;
-  k2.mask_stride = 1;
-  return run_k2(p.dtype, true, k2, st);
+  // rows the partition could not place: the persistent fallback kernel
+  switch (p.dtype) {
+    case F32: return xc::launch_fallback<F32>(a, p.kb, slots, P + p.k, st);
+    case BF16: return xc::launch_fallback<BF16>(a, p.kb, slots, P + p.k, st);
+    default: return xc::launch_fallback<F16>(a, p.kb, slots, P + p.k, st);
+  }
 }
 
 }  // namespace btk

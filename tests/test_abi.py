@@ -66,7 +66,7 @@ _PLANS = [
     (128, 65536, 16384, 2048, 8, _lib.BTK_F32, 1, 1),
     (128, 1 << 20, 256, 512, 1, _lib.BTK_BF16, 1, 1),       # cfg3
     (4096, 32768, 512, 512, 1, _lib.BTK_BF16, 1, 1),        # cfg4: warp-per-row kernel
-    (8192, 1 << 20, 65536, 65536, 2, _lib.BTK_BF16, 1, 3),  # cfg5: cluster exchange + masked fallback K2 x2
+    (8192, 1 << 20, 65536, 65536, 2, _lib.BTK_BF16, 1, 2),  # cfg5: cluster exchange + fallback kernel
 ]
 
 
