@@ -892,6 +892,54 @@ __global__ void __launch_bounds__(NT, 1) fused_wide(WideArgs a) {
   if (!a.early) pdl_wait();
   const bool tr = a.trace && tid == 0 && blockIdx.x < 8192;
   if (tr) g_trace[blockIdx.x][0] = gtime();
+  auto spill_col = [&](Queue<KB> (&q)[V], int64_t g) {
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      const int64_t col = g * V + e;
+#pragma unroll
+      for (int z = 0; z < KB; ++z) {
+        if (z < a.kb) {
+          const int p = (int)(col * a.kb + z);  // bucket-id order
+          pool[a.lsd_lowbit ? lsd::pad32(p) : p] = comp_of<DT>(q[e].v[z], q[e].t[z], col, b, a.geo);
+        }
+      }
+    }
+  };
+  if (s <= U) {
+    // short columns (cfg2: s = 8): one load round per vector column, so
+    // software-pipeline across columns — the next column's loads are in
+    // flight while this one is scanned (2*s loads per thread)
+    auto load_col = [&](uint4 (&v)[U], int64_t g) {
+      const uint8_t* colp = rowp + g * V * ESZ;
+      const int64_t s_eff = (g < a.last_vec) ? s : s - 1;  // ragged final view-row
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        v[u] = (g < a.G && u < s_eff) ? ldg_stream(colp + (int64_t)u * b * ESZ) : make_uint4(0u, 0u, 0u, 0u);
+    };
+    uint4 cur[U], nxt[U];
+    int64_t g = tid;
+    load_col(cur, g);
+    for (; g < a.G; g += NT) {
+      load_col(nxt, g + NT);
+      Queue<KB> q[V];
+#pragma unroll
+      for (int e = 0; e < V; ++e) q[e].init();
+      const int64_t s_eff = (g < a.last_vec) ? s : s - 1;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (u < s_eff) {
+          bad |= nonfinite_bits<DT>(cur[u]);
+          float f[V];
+          unpack<DT>(cur[u], f);
+#pragma unroll
+          for (int e = 0; e < V; ++e) q[e].push(f[e], u);
+        }
+      }
+      spill_col(q, g);
+#pragma unroll
+      for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+    }
+  } else
   for (int64_t g = tid; g < a.G; g += NT) {
     Queue<KB> q[V];
 #pragma unroll
@@ -917,17 +965,7 @@ __global__ void __launch_bounds__(NT, 1) fused_wide(WideArgs a) {
         }
       }
     }
-#pragma unroll
-    for (int e = 0; e < V; ++e) {
-      const int64_t col = g * V + e;
-#pragma unroll
-      for (int z = 0; z < KB; ++z) {
-        if (z < a.kb) {
-          const int p = (int)(col * a.kb + z);  // bucket-id order
-          pool[a.lsd_lowbit ? lsd::pad32(p) : p] = comp_of<DT>(q[e].v[z], q[e].t[z], col, b, a.geo);
-        }
-      }
-    }
+    spill_col(q, g);
   }
   if (tr) g_trace[blockIdx.x][2] = g_trace[blockIdx.x][3] = gtime();
   if (__syncthreads_or(nonfinite_hit<DT>(bad)) && tid == 0 && a.flag) atomicOr(a.flag, 1u);
