@@ -476,6 +476,16 @@ struct Scanner16x2 {
       }
     }
   }
+  // f(i, raw, code) per survivor i = column offset in the group (code
+  // 0xFFFF = empty): the 16-bit value and its view-row, no composite key
+  template <class F>
+  __device__ __forceinline__ void each_raw(F&& f) const {
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) f(2 * w + h, (m2[w] >> (16 * h)) & 0xFFFFu, (c2[w] >> (16 * h)) & 0xFFFFu);
+    }
+  }
 };
 
 template <> struct Scanner<BF16, 1> : Scanner16x2<BF16> {};
@@ -552,6 +562,18 @@ struct Scanner16x2K2 {
           }
           f(col, z, c);
         }
+      }
+    }
+  }
+  // f(i, raw, code) per survivor i = 2 * column offset + z (see Scanner16x2)
+  template <class F>
+  __device__ __forceinline__ void each_raw(F&& f) const {
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        f(2 * (2 * w + h), (m1[w] >> (16 * h)) & 0xFFFFu, (c1[w] >> (16 * h)) & 0xFFFFu);
+        f(2 * (2 * w + h) + 1, (m2[w] >> (16 * h)) & 0xFFFFu, (c2[w] >> (16 * h)) & 0xFFFFu);
       }
     }
   }

@@ -73,6 +73,17 @@ __device__ __forceinline__ void digit_scan(uint32_t* cnt, uint32_t (*ws)[WORDS],
   for (int q = 0; q < WORDS; ++q) cnt[q * NT + tid] = w[q] - own[q] + ws[warp][q];
 }
 
+// digit_scan whose per-thread bases start at off[d] instead of 0 (a
+// running offset per digit across rounds; bases stay below 2^16)
+template <int NT, int WORDS>
+__device__ __forceinline__ void digit_scan_from(uint32_t* cnt, uint32_t (*ws)[WORDS], uint32_t* tot, uint32_t* dex,
+                                                const uint32_t* off) {
+  digit_scan<NT, WORDS>(cnt, ws, tot, dex);
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int q = 0; q < WORDS; ++q) cnt[q * NT + tid] += off[2 * q] | (off[2 * q + 1] << 16);
+}
+
 // count one item of digit d in the thread's counters; returns the number of
 // the thread's earlier items with that digit
 template <int NT>

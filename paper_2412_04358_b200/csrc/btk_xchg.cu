@@ -551,6 +551,499 @@ cudaError_t launch_fallback(const XArgs& a, int64_t kb, uint64_t* slots, int64_t
   return cudaGetLastError();
 }
 
+// ================================================================ batched pipeline
+// The same algorithm without clusters, for 16-bit dtypes: the splitters come
+// from a sampling pass, so the chunks of a row never synchronise with each
+// other — no cluster barriers, and the owner sorts run as independent,
+// fully occupied CTAs.  Intermediates of a batch of rows stay in L2.
+//
+//   xb_split   one CTA per row (all rows, once): Stage 1 of SPC/(V*KB)
+//              sampled column groups per chunk (~3% of the row) gives SPC
+//              sampled candidates per chunk; local quantiles at the owner
+//              boundaries and at the threshold rank, averaged over the C
+//              chunks and rounded down to whole values -> C splitter vkeys.
+//   xb_part    grid (C, BR) per batch: CTA (c, r) runs Stage 1 on chunk c of
+//              row r in shared memory, assigns each candidate its owner
+//              (keys >= spl[1]: owner 0; else a table lookup on the vkey;
+//              below the threshold: none) and scatters the 32-bit sort keys
+//              into its own sub-slot of each owner's segment, stably (bucket
+//              order), with the per-owner counts and the chunk's max vkey.
+//   xb_sort    grid (C, BR) per batch: owner d of row r reads the C x (C+1)
+//              counts, derives the row's verdict and its output offset (the
+//              same in every CTA of the row), gathers its C sub-slots in
+//              chunk order, sorts them (4-bit LSD over the bits above the
+//              bucket id) and emits.  Rows whose verdict fails (sub-slot or
+//              owner overflow, key range, fewer than k kept) go to the
+//              fallback list, finished by xc_fallback after the last batch.
+constexpr int XB_C = 16;       // chunks (= owners) per row
+constexpr int XB_NT = 512;     // threads of every xb CTA
+constexpr int XB_IPT = 16;     // candidates per thread in xb_part (ncand <= 8192)
+constexpr int XB_CAP = 8192;   // keys per owner in xb_sort (NT x ITEMS)
+constexpr int XB_ITEMS = 16;     // (a thread's rank within a digit fits 4 bits)
+
+__host__ __device__ inline int xb_rthr(int64_t k, int64_t P) {
+  const double q = (double)k / (double)P;
+  if (q >= 1.0) return SPC;
+  const double r = SPC * q + 4.0 * sqrt(SPC * q * (1.0 - q) / XB_C) + 0.5;
+  return r >= (double)SPC ? SPC : (int)ceil(r);
+}
+
+struct XBArgs {
+  XArgs x;             // problem, outputs, fallback list
+  int64_t r0;          // first row of the batch
+  int br;              // rows in the batch
+  int capc;            // keys per (owner, chunk) sub-slot
+  uint32_t* spl;       // m x (C+1) splitter vkeys (spl[r][0] unused)
+  uint32_t* seg;       // br x C owners x C chunks x capc sort keys
+  uint32_t* cnt;       // br x C chunks x (C+1): per-owner counts, chunk max vkey
+};
+
+template <int DT, int KB>
+__global__ void __launch_bounds__(XB_NT) xb_split(XBArgs A) {
+  constexpr int V = Vec<DT>::V;
+  constexpr int ESZ = VT<DT>::W / 8;
+  constexpr int C = XB_C, NT = XB_NT;
+  constexpr int G = SPC / (V * KB);  // sampled column groups per chunk
+  static_assert(G >= 1 && G * V * KB == SPC, "sample layout");
+  const XArgs& a = A.x;
+  const int tid = threadIdx.x;
+  const int64_t row = blockIdx.x;
+  const int ib1 = a.geo.ib + 1;
+  __shared__ unsigned long long smp[C][SPC];
+  __shared__ unsigned long long srt[C][SPC];
+  __shared__ unsigned long long est[C][C + 1];
+  pdl_trigger();
+  if (!a.early) pdl_wait();
+  const int span = a.cols / G;  // columns between sampled groups (multiple of V)
+  if (tid < C * G) {
+    const int c = tid / G, g = tid % G;
+    const int off = (int)(((uint64_t)row * 40503u + c * 977u + g * 7u) % (uint64_t)(span / V)) * V;
+    const int64_t col = (int64_t)c * a.cols + (int64_t)g * span + off;
+    const uint8_t* colp = static_cast<const uint8_t*>(a.x) + (row * a.row_stride + col) * ESZ;
+    Scanner<DT, KB> sc;
+    sc.init();
+    for (int t = 0; t < a.s; ++t) sc.row(ldg_stream(colp + (int64_t)t * a.b * ESZ), t);
+    sc.each_comp((int)(col / V), a.b, 0, a.geo, [&](int64_t cc, int z, uint64_t comp) {
+      smp[c][g * V * KB + (int)(cc - col) * KB + z] = comp;
+    });
+  }
+  __syncthreads();
+  for (int i = tid; i < C * SPC; i += NT) {
+    const int c = i / SPC;
+    const unsigned long long x = smp[c][i % SPC];
+    int r = 0;
+#pragma unroll 8
+    for (int q = 0; q < SPC; ++q) r += smp[c][q] > x ? 1 : 0;
+    srt[c][r] = x;
+  }
+  __syncthreads();
+  const int rthr = xb_rthr(a.k, a.b * KB);
+  for (int i = tid; i < C * C; i += NT) {
+    const int c = i / C, q = 1 + i % C;
+    if (q < C) {  // local quantile at the fractional rank q * rthr / C (linear in comp space)
+      const int p256 = (q * rthr * 256) / C;
+      const int r0 = p256 >> 8, f = p256 & 255;
+      const unsigned long long hi = srt[c][r0], lo = srt[c][r0 + 1 < SPC ? r0 + 1 : r0];
+      est[c][q] = hi - (((hi - lo) * (unsigned long long)f) >> 8);
+    } else {
+      est[c][q] = srt[c][rthr < SPC ? rthr : SPC - 1];
+    }
+  }
+  __syncthreads();
+  // Splitters are "fine keys": the value key with the top TB bits of the
+  // view-row below it, fk = vkey << TB | (2^TB - 1 - (t >> (tbits - TB))),
+  // ordered like the composite keys.  Whole values alone are too coarse
+  // when one 16-bit value holds a large share of an owner's keys; TB is the
+  // most view-row bits for which the owner table over [spl[C], spl[1])
+  // still fits LUTN entries.
+  __shared__ unsigned long long avg[C + 1];
+  __shared__ int s_tb;
+  if (tid > 0 && tid <= C) {
+    unsigned long long sum = 0;
+    for (int c = 0; c < C; ++c) sum += est[c][tid];
+    avg[tid] = sum / C;
+  }
+  __syncthreads();
+  const int tbits = a.geo.ib - a.logb;  // view-row bits of any index field
+  if (tid == 0) {
+    const uint32_t vspan = (uint32_t)(avg[1] >> ib1) - (uint32_t)(avg[C] >> ib1) + 1u;
+    int tb = tbits;
+    while (tb > 0 && ((uint64_t)vspan << tb) > (uint64_t)LUTN) --tb;
+    s_tb = tb;
+  }
+  __syncthreads();
+  pdl_wait_writes(a.early != 0);
+  if (tid <= C) {
+    const int tb = s_tb;
+    uint32_t v = (uint32_t)tb;  // slot 0: TB
+    if (tid > 0) {
+      const unsigned long long c = avg[tid];
+      const uint32_t idx = a.geo.imax - (uint32_t)((c >> 1) & a.geo.imax);
+      v = ((uint32_t)(c >> ib1) << tb) | (((1u << tb) - 1u) - ((idx >> a.logb) >> (tbits - tb)));
+    }
+    A.spl[row * (C + 1) + tid] = v;
+  }
+}
+
+// survivors of one scanned column group as (item, vkey, view-row, negzero);
+// item = column offset in the group * KB + z
+template <int DT, int KB, class F>
+__device__ __forceinline__ void xb_each_rec(const Scanner<DT, KB>& sc, int g, const XArgs& a, F&& f) {
+  if constexpr (DT != F32 && KB <= 2) {
+    sc.each_raw([&](int i, uint32_t raw, uint32_t code) {
+      f(i, vkey<DT>(raw), code, is_negzero<DT>(raw), code != 0xFFFFu);
+    });
+  } else {
+    constexpr int V = Vec<DT>::V;
+    sc.each_comp(g, a.b, 0, a.geo, [&](int64_t col, int z, uint64_t c) {
+      const uint32_t idx = a.geo.imax - (uint32_t)((c >> 1) & a.geo.imax);
+      f((int)(col - (int64_t)g * V) * KB + z, (uint32_t)(c >> (a.geo.ib + 1)), idx >> a.logb, (uint32_t)(c & 1u),
+        c != 0ull);
+    });
+  }
+}
+
+template <int DT, int KB>
+__global__ void __launch_bounds__(XB_NT, 2) xb_part(XBArgs A) {
+  constexpr int V = Vec<DT>::V;
+  constexpr int ESZ = VT<DT>::W / 8;
+  constexpr int C = XB_C, NT = XB_NT, NW = NT / 32;
+  constexpr int IT = V * KB;  // survivors per column group (one group per thread and round)
+  constexpr int U = KB >= 2 ? 4 : 8;  // 16-byte loads in flight (register budget of 64)
+  const XArgs& a = A.x;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int c = blockIdx.x, rl = blockIdx.y;
+  const int64_t row = A.r0 + rl;
+  const int64_t col0 = (int64_t)c * a.cols;
+  const int gv = a.cols / V;
+  const int ib1 = a.geo.ib + 1;
+  extern __shared__ __align__(128) uint8_t xsm[];
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(xsm);  // [8][NT] digit counters
+  __shared__ uint8_t lut[LUTN];
+  __shared__ uint32_t ws[NW][8];
+  __shared__ uint32_t sendcnt[16], dex[16], run[16];
+  __shared__ uint32_t lspl[C + 1], kofs[C];
+  __shared__ uint32_t s_max;
+  if (tid == 0) s_max = 0u;
+  if (tid < 16) run[tid] = 0u;
+  pdl_trigger();
+  if (!a.early) pdl_wait();
+  uint32_t bad = 0, mx = 0;
+  uint32_t vthr = 0, tmax = 0;
+  int tb = 0, tsh = 0;
+  const uint8_t* rowp = static_cast<const uint8_t*>(a.x) + (row * a.row_stride + col0) * ESZ;
+  const int64_t vstride = a.b * ESZ;
+  uint32_t* seg = A.seg + ((int64_t)rl * C * C + c) * A.capc;  // + owner * C * capc
+  const uint32_t ostride = (uint32_t)(C * A.capc);  // owner stride in the row-chunk's sub-slots
+  const uint32_t capc = (uint32_t)A.capc;
+  const int lb1 = a.logb + 1;
+  for (int g0 = 0; g0 < gv; g0 += NT) {  // rounds: groups g0 + tid, in bucket order
+    const int g = g0 + tid;
+    const bool act = g < gv;
+    // ---- Stage 1 of one column group (V buckets) in registers
+    Scanner<DT, KB> sc;
+    sc.init();
+    if (act) {
+      // 32-bit row offsets (s * b * ESZ < 4 GB): one pointer, no 64-bit
+      // address arithmetic per load
+      const uint8_t* colp = rowp + (int64_t)g * V * ESZ;
+      const uint32_t vs = (uint32_t)vstride;
+      int t0 = 0;
+      for (; t0 + U <= a.s; t0 += U) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = ldg_stream(colp + (uint32_t)(t0 + u) * vs);
+#pragma unroll
+        for (int u = 0; u < U; ++u) sc.row(v[u], t0 + u);
+      }
+      for (; t0 < a.s; ++t0) sc.row(ldg_stream(colp + (uint32_t)t0 * vs), t0);
+      bad |= sc.nonfinite() ? 1u : 0u;
+    }
+    // every bucket has >= k_b survivors (planner: s >= k_b), so an active
+    // thread's items are all real
+    uint32_t rec[IT];  // vkey << 16 | (rank among the thread's items of its owner) << 11 | view-row << 1 | negzero
+    xb_each_rec<DT, KB>(sc, (int)(col0 / V) + g, a, [&](int i, uint32_t vk, uint32_t t, uint32_t nz, bool) {
+      rec[i] = (vk << 16) | (t << 1) | nz;
+      mx = act && vk > mx ? vk : mx;
+    });
+    if (g0 == 0) {
+      // the splitters (xb_split) and this batch's buffers (the previous
+      // batch's sort) are ready once the predecessor completed
+      pdl_wait_writes(a.early != 0);
+      if (tid <= C) lspl[tid] = A.spl[row * (C + 1) + tid];
+      __syncthreads();
+      tb = (int)lspl[0];
+      tsh = a.geo.ib - a.logb - tb;
+      tmax = (1u << tb) - 1u;
+      // owner table over fine keys [spl[C], spl[C] + LUTN): owners 1..C-1
+      // below spl[1], owner 0 from spl[1] up (beyond the table: owner 0 too)
+      vthr = lspl[C];
+      const uint32_t vspan = lspl[1] - lspl[C];
+      for (uint32_t w = tid; w < (uint32_t)LUTN / 4; w += NT) {
+        uint32_t word = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t i = 4 * w + e;
+          uint32_t o = 0;
+          if (i < vspan) {
+            const uint32_t v = vthr + i;
+            o = 1;
+#pragma unroll
+            for (int q = 2; q < C; ++q) o += lspl[q] > v ? 1u : 0u;
+          }
+          word |= o << (8 * e);
+        }
+        reinterpret_cast<uint32_t*>(lut)[w] = word;
+      }
+      if (tid < C) kofs[tid] = (lspl[tid + 1] >> tb) << ib1;
+    }
+    // ---- owners, stable ranks (thread-blocked items), scatter into sub-slots.
+    // The item's rank among the thread's earlier items of its owner goes to
+    // bits 11..15 of its record (view-rows < 1024); the owner is looked up
+    // again after the scan (no second per-item register array).
+    auto owner = [&](uint32_t r, bool ok) -> uint32_t {
+      const uint32_t vk = ((r >> 16) << tb) | (tmax - (((r >> 1) & 0x3FFu) >> tsh));  // fine key
+      const uint32_t off = vk - vthr;  // wraps below the threshold
+      uint32_t d = vk < vthr ? (uint32_t)C : 0u;
+      if (off < (uint32_t)LUTN) d = lut[off];
+      return ok ? d : (uint32_t)C;
+    };
+#pragma unroll
+    for (int q = 0; q < 8; ++q) cnt[q * NT + tid] = 0u;
+    __syncthreads();  // table built; counters of the previous round consumed
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+      const uint32_t d = owner(rec[i], act);
+      if (d < (uint32_t)C) rec[i] |= lsd::count_digit<NT>(cnt, d) << 11;
+    }
+    lsd::digit_scan_from<NT, 8>(cnt, ws, sendcnt, dex, run);
+    // key = (vkey - spl[d+1]) << ib1 | (imax - idx) << 1 | negzero with
+    // idx = view-row << logb | bucket, as one sum of its disjoint fields
+    const uint32_t kb0 = 2u * (a.geo.imax - (uint32_t)(col0 + (int64_t)g * V));
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+      const uint32_t d = owner(rec[i], act);
+      const uint32_t dd = d < (uint32_t)C ? d : 0u;  // in-range reads for unselected items
+      const uint32_t pos = lsd::digit_base<NT>(cnt, dd) + ((rec[i] >> 11) & 31u);
+      const uint32_t key = ((rec[i] >> 16) << ib1) - kofs[dd] + kb0 - 2u * (uint32_t)(i / KB) -
+                           (((rec[i] >> 1) & 0x3FFu) << lb1) + (rec[i] & 1u);
+      if (d < (uint32_t)C && pos < capc) seg[dd * ostride + pos] = key;
+    }
+    __syncthreads();
+    if (tid < C) run[tid] += sendcnt[tid];
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+  if (lane == 0) atomicMax(&s_max, mx);
+  if (__syncthreads_or(bad) && tid == 0 && a.flag) atomicOr(a.flag, 1u);
+  uint32_t* cn = A.cnt + ((int64_t)rl * C + c) * (C + 1);
+  if (tid < C) cn[tid] = run[tid];
+  if (tid == C) cn[C] = s_max;
+}
+
+template <int DT>
+__global__ void __launch_bounds__(XB_NT, 2) xb_sort(XBArgs A) {
+  using KT = uint32_t;
+  constexpr int NT = XB_NT, NW = NT / 32, ITEMS = XB_ITEMS, C = XB_C;
+  const XArgs& a = A.x;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int d = blockIdx.x, rl = blockIdx.y;
+  const int64_t row = A.r0 + rl;
+  const int ib1 = a.geo.ib + 1;
+  extern __shared__ __align__(128) uint8_t xsm[];
+  KT* buf = reinterpret_cast<KT*>(xsm);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(buf + padk<KT>(XB_CAP));
+  __shared__ uint32_t ws[NW][8];
+  __shared__ uint32_t dtot[16], dex[16];
+  __shared__ uint32_t cn[C][C + 1];
+  __shared__ uint32_t lspl[C + 1];
+  __shared__ uint32_t tot[C], pre[C + 1];
+  __shared__ uint32_t s_vary, s_and, s_mx;
+  __shared__ int s_why;
+  __shared__ uint32_t s_start;
+  pdl_trigger();
+  pdl_wait();  // the partition launch produced the counts and sub-slots
+  for (int i = tid; i < C * (C + 1); i += NT) cn[i / (C + 1)][i % (C + 1)] = A.cnt[(int64_t)rl * C * (C + 1) + i];
+  if (tid <= C) lspl[tid] = A.spl[row * (C + 1) + tid];
+  if (tid == 0) { s_vary = 0u; s_and = ~0u; }
+  __syncthreads();
+  if (tid < C) {
+    uint32_t t = 0;
+    for (int c = 0; c < C; ++c) t += cn[c][tid];
+    tot[tid] = t;
+  } else if (tid == C) {
+    uint32_t m = 0;
+    for (int c = 0; c < C; ++c) m = max(m, cn[c][C]);
+    s_mx = m;
+  }
+  const int over = __syncthreads_or(tid < C * C && cn[tid / C][tid % C] > (uint32_t)A.capc);
+  if (tid == 0) {  // verdict (identical in every CTA of the row) and offsets
+    int why = over ? 1 : 0;
+    uint32_t sum = 0;
+    const int tb = (int)lspl[0];
+    for (int q = 0; q < C; ++q) {
+      if (q == d) s_start = sum;
+      sum += tot[q];
+      if (tot[q] > (uint32_t)XB_CAP) why |= 1;
+      // the owner's value offsets must fit the 32-bit key above the index field
+      const uint32_t hi = q == 0 ? s_mx : (lspl[q] - 1u) >> tb;
+      if (tot[q] && ((uint64_t)(hi - (lspl[q + 1] >> tb)) >> (32 - ib1)) != 0ull) why |= 2;
+    }
+    if (lspl[1] - lspl[C] > (uint32_t)LUTN) why |= 2;
+    if (sum < (uint64_t)a.k) why |= 4;
+    if (why && d == 0) a.fb_list[atomicAdd(a.fb_count, 1)] = (int)row;
+    s_why = why;
+    uint32_t p = 0;
+    for (int c = 0; c < C; ++c) {
+      pre[c] = p;
+      p += cn[c][d];
+    }
+    pre[C] = p;
+  }
+  __syncthreads();
+  const int R = (int)tot[d];
+  const int64_t start = s_start;
+  if (s_why || R == 0 || start >= a.k) return;
+  // ---- gather the C sub-slots in chunk order (bucket order within a
+  // chunk) straight into registers, thread-blocked: position p = tid*items+i
+  const int items = (R + NT - 1) / NT;
+  KT key[ITEMS];
+  {
+    const uint32_t* seg = A.seg + ((int64_t)rl * C + d) * C * A.capc;
+    const int p0 = tid * items;
+    int cc = 0;  // sub-slot holding p0: the last with pre[cc] <= p0
+#pragma unroll
+    for (int st = C / 2; st > 0; st >>= 1)
+      if (pre[cc + st] <= (uint32_t)p0) cc += st;
+    KT kor = 0, kand = ~(KT)0;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      key[i] = 0;  // pads sort last
+      const int p = p0 + i;
+      if (i < items && p < R) {
+        while (pre[cc + 1] <= (uint32_t)p) ++cc;
+        key[i] = seg[(int64_t)cc * A.capc + (p - (int)pre[cc])];
+        kor |= key[i];
+        kand &= key[i];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      kor |= __shfl_xor_sync(0xFFFFFFFFu, kor, o);
+      kand &= __shfl_xor_sync(0xFFFFFFFFu, kand, o);
+    }
+    if (lane == 0) {
+      atomicOr(&s_vary, (uint32_t)kor);
+      atomicAnd(&s_and, (uint32_t)kand);
+    }
+  }
+  __syncthreads();
+  // ---- 4-bit LSD passes over the bits above the bucket id that vary (keys
+  // in registers, one shared buffer); buf ends in sorted order
+  const KT vary = s_vary ^ s_and;
+  const int lowbit = 1 + a.logb;
+  int shift = lowbit;
+  if ((vary >> lowbit) != 0) shift = lowbit + __ffs((int)(vary >> lowbit)) - 1;
+  bool none = true;
+  for (; shift < 32 && (vary >> shift) != 0; shift += 4) {
+    if (((vary >> shift) & (KT)0xF) == 0) continue;
+    if (!none) {
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i)
+        if (i < items) key[i] = buf[padk<KT>(tid * items + i)];
+    }
+    none = false;
+    uint32_t sl[ITEMS / 4];  // per item one byte: digit << 4 | rank among the thread's items of that digit
+#pragma unroll
+    for (int q = 0; q < ITEMS / 4; ++q) sl[q] = 0u;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) cnt[q * NT + tid] = 0u;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      if (i < items) {
+        const uint32_t dg = 15u - (uint32_t)((key[i] >> shift) & (KT)0xF);
+        sl[i / 4] |= ((dg << 4) | lsd::count_digit<NT>(cnt, dg)) << (8 * (i % 4));
+      }
+    }
+    lsd::digit_scan<NT, 8>(cnt, ws, dtot, dex);  // its barriers order every read of buf before the stores
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      if (i < items) {
+        const uint32_t b8 = (sl[i / 4] >> (8 * (i % 4))) & 0xFFu;
+        const uint32_t dg = b8 >> 4;
+        const int r = (int)(dex[dg] + lsd::digit_base<NT>(cnt, dg) + (b8 & 0xFu));
+        buf[padk<KT>(r)] = key[i];
+      }
+    }
+    __syncthreads();
+  }
+  if (none) {  // already in order
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i)
+      if (i < items) buf[padk<KT>(tid * items + i)] = key[i];
+    __syncthreads();
+  }
+  const KT* src = buf;
+  const int keep = (int)min((int64_t)R, a.k - start);
+  const uint32_t vbase = lspl[d + 1] >> (int)lspl[0];
+  for (int q = tid; q < keep; q += NT) {
+    const KT key = src[padk<KT>(q)];
+    const uint64_t cc = ((uint64_t)(vbase + (key >> ib1)) << ib1) | (uint64_t)(key & ((1u << ib1) - 1u));
+    emit_comp<DT>(cc, row * a.k + start + q, a.geo, a.out_vals, a.out_idx);
+  }
+}
+
+constexpr size_t XB_PART_SMEM = (size_t)8 * XB_NT * 4;
+constexpr size_t XB_SORT_SMEM = (size_t)padk<uint32_t>(XB_CAP) * 4 + (size_t)8 * XB_NT * 4;
+
+inline int xb_rows(int64_t m) { return (int)std::min<int64_t>(m, std::max(1, fz::env_int("BTK_XB_ROWS", 64))); }
+
+template <int DT, int KB>
+cudaError_t xb_attrs() {
+  static thread_local int attr_done = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_done == dev) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute((const void*)xb_sort<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)XB_SORT_SMEM);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute((const void*)xb_part<DT, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)XB_PART_SMEM);
+  if (e != cudaSuccess) return e;
+  attr_done = dev;
+  return cudaSuccess;
+}
+
+template <int DT, int KB>
+cudaError_t xb_launch_all(XBArgs A, cudaStream_t st) {
+  cudaError_t e = xb_attrs<DT, KB>();
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.stream = st;
+  cfg.blockDim = dim3(XB_NT);
+  cfg.gridDim = dim3((unsigned)A.x.m);
+  e = cudaLaunchKernelEx(&cfg, xb_split<DT, KB>, A);
+  if (e != cudaSuccess) return e;
+  const int br = xb_rows(A.x.m);
+  for (int64_t r0 = 0; r0 < A.x.m; r0 += br) {
+    A.r0 = r0;
+    A.br = (int)std::min<int64_t>(br, A.x.m - r0);
+    cfg.gridDim = dim3(XB_C, (unsigned)A.br);
+    cfg.dynamicSmemBytes = XB_PART_SMEM;
+    e = cudaLaunchKernelEx(&cfg, xb_part<DT, KB>, A);
+    if (e != cudaSuccess) return e;
+    cfg.dynamicSmemBytes = XB_SORT_SMEM;
+    e = cudaLaunchKernelEx(&cfg, xb_sort<DT>, A);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 // ================================================================ host side
 template <int DT> struct Cfg;
 template <> struct Cfg<F32> {
@@ -673,12 +1166,58 @@ bool xchg_supported(const Problem& p) {
 
 static size_t al256(size_t v) { return (v + 255) & ~(size_t)255; }
 
+namespace xc {
+// batched pipeline (16-bit dtypes): BTK_XB=1 selects it over the cluster kernel
+inline bool use_batched(const Problem& p) { return p.dtype != F32 && fz::env_int("BTK_XB", 0) == 1; }
+
+inline int xb_capc(const Problem& p, int ncand) {
+  // expected keys per (owner, chunk): the kept fraction of the chunk over C
+  // owners; 2x plus a margin (owners vary by whole values and by the
+  // sampling error of the splitters), rounded to whole 128-byte lines
+  const double e = (double)xb_rthr(p.k, p.b * p.kb) / SPC * ncand / XB_C;
+  const int c = ((int)(2.0 * e) + 128 + 31) & ~31;
+  return std::min(c, XB_CAP);
+}
+
+struct XBBufs {
+  size_t spl, seg, cnt, total;
+};
+inline XBBufs xb_bufs(const Problem& p) {
+  const size_t br = (size_t)xb_rows(p.m);
+  const int ncand = (int)(p.b / XB_C * p.kb);
+  XBBufs u{};
+  u.spl = al256((size_t)p.m * (XB_C + 1) * 4);
+  u.seg = al256(br * XB_C * XB_C * (size_t)xb_capc(p, ncand) * 4);
+  u.cnt = al256(br * XB_C * (XB_C + 1) * 4);
+  u.total = u.spl + u.seg + u.cnt;
+  return u;
+}
+
+template <int DT>
+cudaError_t run_batched(const Problem& p, const XArgs& a, uint8_t* w, cudaStream_t st) {
+  const XBBufs u = xb_bufs(p);
+  XBArgs A{};
+  A.x = a;
+  A.capc = xb_capc(p, a.ncand);
+  A.spl = reinterpret_cast<uint32_t*>(w);
+  A.seg = reinterpret_cast<uint32_t*>(w + u.spl);
+  A.cnt = reinterpret_cast<uint32_t*>(w + u.spl + u.seg);
+  switch (p.kb) {
+    case 1: return xb_launch_all<DT, 1>(A, st);
+    case 2: return xb_launch_all<DT, 2>(A, st);
+    case 4: return xb_launch_all<DT, 4>(A, st);
+  }
+  return cudaErrorNotSupported;
+}
+}  // namespace xc
+
 size_t xchg_workspace_bytes(const Problem& p) {
-  // fallback-row counter + list, and one scratch slot (pool + k keys) per
-  // fallback CTA
+  // fallback-row counter + list, one scratch slot (pool + k keys) per
+  // fallback CTA, and the batched pipeline's per-batch buffers
   const int64_t P = p.b * p.kb;
   const int64_t ctas = std::min<int64_t>(p.m, xc::FB_CTAS);
-  return al256(4) + al256((size_t)p.m * 4) + al256((size_t)ctas * (P + p.k) * 8);
+  const size_t xb = xc::use_batched(p) ? xc::xb_bufs(p).total : 0;
+  return al256(4) + al256((size_t)p.m * 4) + al256((size_t)ctas * (P + p.k) * 8) + xb;
 }
 
 cudaError_t run_xchg(const Problem& p, void* ws, void* out_vals, int64_t* out_idx, cudaStream_t st) {
@@ -699,7 +1238,11 @@ cudaError_t run_xchg(const Problem& p, void* ws, void* out_vals, int64_t* out_id
   a.early = (p.flags & 1u) && fz::pdl_enabled() ? 1 : 0;
   cudaError_t e = cudaMemsetAsync(count, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
-  switch (p.dtype) {
+  const int64_t ctas = std::min<int64_t>(p.m, xc::FB_CTAS);
+  uint8_t* xbw = reinterpret_cast<uint8_t*>(slots) + al256((size_t)ctas * (P + p.k) * 8);
+  switch (xc::use_batched(p) ? -p.dtype - 1 : p.dtype) {
+    case -BF16 - 1: e = xc::run_batched<BF16>(p, a, xbw, st); break;
+    case -F16 - 1: e = xc::run_batched<F16>(p, a, xbw, st); break;
     case F32: e = xc::launch_dt<F32>(a, p.kb, st); break;
     case BF16: e = xc::launch_dt<BF16>(a, p.kb, st); break;
     case F16: e = xc::launch_dt<F16>(a, p.kb, st); break;
