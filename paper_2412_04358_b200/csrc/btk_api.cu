@@ -217,8 +217,9 @@ int btk_launch_count(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, int
     p.x = reinterpret_cast<const void*>(uintptr_t(256));
     p.row_stride = row_stride; p.dtype = dtype;
     p.m = m; p.n = n; p.k = k; p.b = b; p.kb = kb; p.layout = layout; p.geo = geo_for(dtype, n);
-    // fused_xchg + the persistent fallback kernel (exits at once without overflow rows)
-    if (xchg_supported(p)) return 2;
+    // the exchange pipeline + the persistent fallback kernel (exits at once
+    // without overflow rows)
+    if (xchg_supported(p)) return xchg_launch_count(p);
   }
   if (btk_uses_fused_path(m, n, k, b, kb, dtype, layout, row_stride)) return 1;
   if (dtype == BTK_F64) {

@@ -104,6 +104,10 @@ cudaError_t run_stage1_vec(const Problem& p, uint64_t* pool, cudaStream_t st,
 // Cluster-exchange fused kernel for large pools (btk_xchg.cu): Stage 1 and
 // Stage 2 of a row in one cluster launch, plus the row-masked generic
 // fallback for rows whose value partition overflows.
+// kernel launches of one call on the exchange family: the batched pipeline
+// (split, then partition + sort per batch of rows, fallback) or the cluster
+// kernel + fallback
+int xchg_launch_count(const Problem& p);
 bool xchg_supported(const Problem& p);
 size_t xchg_workspace_bytes(const Problem& p);
 cudaError_t run_xchg(const Problem& p, void* ws, void* out_vals, int64_t* out_idx, cudaStream_t st);

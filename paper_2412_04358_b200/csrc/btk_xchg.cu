@@ -45,6 +45,8 @@
 // position, and the sort key is (comp - base_r) in 32 bits, base_r the
 // owner's range floor aligned to the value field; fp32 uses the 64-bit
 // composite key (btk_common.cuh) throughout.
+#include <unordered_map>
+
 #include "btk_fused_impl.cuh"
 #include "btk_k2dev.cuh"
 
@@ -578,8 +580,11 @@ cudaError_t launch_fallback(const XArgs& a, int64_t kb, uint64_t* slots, int64_t
 constexpr int XB_C = 16;       // chunks (= owners) per row
 constexpr int XB_NT = 512;     // threads of every xb CTA
 constexpr int XB_IPT = 16;     // candidates per thread in xb_part (ncand <= 8192)
-constexpr int XB_CAP = 8192;   // keys per owner in xb_sort (NT x ITEMS)
-constexpr int XB_ITEMS = 16;     // (a thread's rank within a digit fits 4 bits)
+constexpr int XB_CAP = 8192;   // keys per owner in xb_sort (SNT x ITEMS)
+constexpr int XB_SNT = 512;    // threads of an owner sort (256 x 32 items: fewer scan
+                               // instructions but 80 registers, lower occupancy: slower)
+constexpr int XB_ITEMS = XB_CAP / XB_SNT;
+constexpr int XB_SMIN = 2;     // resident sorts per SM (64 registers)
 
 __host__ __device__ inline int xb_rthr(int64_t k, int64_t P) {
   const double q = (double)k / (double)P;
@@ -596,6 +601,7 @@ struct XBArgs {
   uint32_t* spl;       // m x (C+1) splitter vkeys (spl[r][0] unused)
   uint32_t* seg;       // br x C owners x C chunks x capc sort keys
   uint32_t* cnt;       // br x C chunks x (C+1): per-owner counts, chunk max vkey
+  size_t seg_elems, cnt_elems;  // one buffer of each (two with the side stream)
 };
 
 template <int DT, int KB>
@@ -842,9 +848,9 @@ __global__ void __launch_bounds__(XB_NT, 2) xb_part(XBArgs A) {
 }
 
 template <int DT>
-__global__ void __launch_bounds__(XB_NT, 2) xb_sort(XBArgs A) {
+__global__ void __launch_bounds__(XB_SNT, XB_SMIN) xb_sort(XBArgs A) {
   using KT = uint32_t;
-  constexpr int NT = XB_NT, NW = NT / 32, ITEMS = XB_ITEMS, C = XB_C;
+  constexpr int NT = XB_SNT, NW = NT / 32, ITEMS = XB_ITEMS, C = XB_C;
   const XArgs& a = A.x;
   const int tid = threadIdx.x, lane = tid & 31;
   const int d = blockIdx.x, rl = blockIdx.y;
@@ -953,25 +959,28 @@ __global__ void __launch_bounds__(XB_NT, 2) xb_sort(XBArgs A) {
         if (i < items) key[i] = buf[padk<KT>(tid * items + i)];
     }
     none = false;
-    uint32_t sl[ITEMS / 4];  // per item one byte: digit << 4 | rank among the thread's items of that digit
+    // per item FB bits: digit << (FB - 4) | rank among the thread's items of that digit
+    constexpr int FB = ITEMS <= 16 ? 8 : 10, RM = (1 << (FB - 4)) - 1;
+    constexpr int SPW = 32 / FB, SLW = (ITEMS + SPW - 1) / SPW;
+    uint32_t sl[SLW];
 #pragma unroll
-    for (int q = 0; q < ITEMS / 4; ++q) sl[q] = 0u;
+    for (int q = 0; q < SLW; ++q) sl[q] = 0u;
 #pragma unroll
     for (int q = 0; q < 8; ++q) cnt[q * NT + tid] = 0u;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       if (i < items) {
         const uint32_t dg = 15u - (uint32_t)((key[i] >> shift) & (KT)0xF);
-        sl[i / 4] |= ((dg << 4) | lsd::count_digit<NT>(cnt, dg)) << (8 * (i % 4));
+        sl[i / SPW] |= ((dg << (FB - 4)) | lsd::count_digit<NT>(cnt, dg)) << (FB * (i % SPW));
       }
     }
     lsd::digit_scan<NT, 8>(cnt, ws, dtot, dex);  // its barriers order every read of buf before the stores
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       if (i < items) {
-        const uint32_t b8 = (sl[i / 4] >> (8 * (i % 4))) & 0xFFu;
-        const uint32_t dg = b8 >> 4;
-        const int r = (int)(dex[dg] + lsd::digit_base<NT>(cnt, dg) + (b8 & 0xFu));
+        const uint32_t bf = (sl[i / SPW] >> (FB * (i % SPW))) & ((1u << FB) - 1u);
+        const uint32_t dg = bf >> (FB - 4);
+        const int r = (int)(dex[dg] + lsd::digit_base<NT>(cnt, dg) + (bf & (uint32_t)RM));
         buf[padk<KT>(r)] = key[i];
       }
     }
@@ -994,9 +1003,15 @@ __global__ void __launch_bounds__(XB_NT, 2) xb_sort(XBArgs A) {
 }
 
 constexpr size_t XB_PART_SMEM = (size_t)8 * XB_NT * 4;
-constexpr size_t XB_SORT_SMEM = (size_t)padk<uint32_t>(XB_CAP) * 4 + (size_t)8 * XB_NT * 4;
+constexpr size_t XB_SORT_SMEM = (size_t)padk<uint32_t>(XB_CAP) * 4 + (size_t)8 * XB_SNT * 4;
 
-inline int xb_rows(int64_t m) { return (int)std::min<int64_t>(m, std::max(1, fz::env_int("BTK_XB_ROWS", 64))); }
+// rows per batch: at most 148 (measured best of 32/64/148 on cfg5); the
+// workspace is sized for the cap, BTK_XB_ROWS may only lower it
+constexpr int XB_ROWS_CAP = 148;
+inline int xb_rows_cap(int64_t m) { return (int)std::min<int64_t>(m, XB_ROWS_CAP); }
+inline int xb_rows(int64_t m) {
+  return std::min(xb_rows_cap(m), std::max(1, fz::env_int("BTK_XB_ROWS", XB_ROWS_CAP)));
+}
 
 template <int DT, int KB>
 cudaError_t xb_attrs() {
@@ -1014,6 +1029,33 @@ cudaError_t xb_attrs() {
   return cudaSuccess;
 }
 
+// Side stream for the owner sorts (per host thread and device): batch i's
+// sort overlaps batch i+1's partition; the partition and sort buffers are
+// double-buffered, so partition i+2 waits for sort i only.
+struct XBSide {
+  cudaStream_t s = nullptr;
+  cudaEvent_t part[2] = {nullptr, nullptr}, sort[2] = {nullptr, nullptr}, fork = nullptr;
+};
+inline cudaError_t xb_side(XBSide*& out) {
+  static thread_local std::unordered_map<int, XBSide> side;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  XBSide& x = side[dev];
+  if (!x.s) {
+    e = cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+      e = cudaEventCreateWithFlags(&x.part[i], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x.sort[i], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  }
+  out = &x;
+  return cudaSuccess;
+}
+inline bool xb_two_streams() { return fz::env_int("BTK_XB_STREAMS", 1) != 0; }
+
 template <int DT, int KB>
 cudaError_t xb_launch_all(XBArgs A, cudaStream_t st) {
   cudaError_t e = xb_attrs<DT, KB>();
@@ -1030,16 +1072,55 @@ cudaError_t xb_launch_all(XBArgs A, cudaStream_t st) {
   e = cudaLaunchKernelEx(&cfg, xb_split<DT, KB>, A);
   if (e != cudaSuccess) return e;
   const int br = xb_rows(A.x.m);
-  for (int64_t r0 = 0; r0 < A.x.m; r0 += br) {
-    A.r0 = r0;
-    A.br = (int)std::min<int64_t>(br, A.x.m - r0);
+  const int64_t nbatch = (A.x.m + br - 1) / br;
+  XBSide* sd = nullptr;
+  const bool two = xb_two_streams() && nbatch > 1;
+  if (two) {
+    e = xb_side(sd);
+    if (e != cudaSuccess) return e;
+    e = cudaEventRecord(sd->fork, st);  // the side stream joins st's work (and a capture) here
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sd->s, sd->fork, 0);
+    if (e != cudaSuccess) return e;
+  }
+  uint32_t* seg0 = A.seg;
+  uint32_t* cnt0 = A.cnt;
+  for (int64_t i = 0; i < nbatch; ++i) {
+    const int buf = two ? (int)(i & 1) : 0;
+    A.r0 = i * br;
+    A.br = (int)std::min<int64_t>(br, A.x.m - A.r0);
+    A.seg = seg0 + (size_t)buf * A.seg_elems;
+    A.cnt = cnt0 + (size_t)buf * A.cnt_elems;
     cfg.gridDim = dim3(XB_C, (unsigned)A.br);
+    cfg.blockDim = dim3(XB_NT);
     cfg.dynamicSmemBytes = XB_PART_SMEM;
+    cfg.stream = st;
+    if (two && i >= 2) {
+      e = cudaStreamWaitEvent(st, sd->sort[buf], 0);  // sort i-2 released this buffer
+      if (e != cudaSuccess) return e;
+    }
     e = cudaLaunchKernelEx(&cfg, xb_part<DT, KB>, A);
     if (e != cudaSuccess) return e;
     cfg.dynamicSmemBytes = XB_SORT_SMEM;
-    e = cudaLaunchKernelEx(&cfg, xb_sort<DT>, A);
+    cfg.blockDim = dim3(XB_SNT);
+    if (two) {
+      e = cudaEventRecord(sd->part[buf], st);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(sd->s, sd->part[buf], 0);
+      if (e != cudaSuccess) return e;
+      cfg.stream = sd->s;
+      cfg.numAttrs = 0;  // fully ordered after its partition (event)
+      e = cudaLaunchKernelEx(&cfg, xb_sort<DT>, A);
+      cfg.numAttrs = pdl_enabled() ? 1 : 0;
+      if (e == cudaSuccess) e = cudaEventRecord(sd->sort[buf], sd->s);
+    } else {
+      e = cudaLaunchKernelEx(&cfg, xb_sort<DT>, A);
+    }
     if (e != cudaSuccess) return e;
+  }
+  if (two) {  // join: st continues after the last sorts
+    for (int b = 0; b < 2; ++b) {
+      e = cudaStreamWaitEvent(st, sd->sort[b], 0);
+      if (e != cudaSuccess) return e;
+    }
   }
   return cudaSuccess;
 }
@@ -1167,8 +1248,9 @@ bool xchg_supported(const Problem& p) {
 static size_t al256(size_t v) { return (v + 255) & ~(size_t)255; }
 
 namespace xc {
-// batched pipeline (16-bit dtypes): BTK_XB=1 selects it over the cluster kernel
-inline bool use_batched(const Problem& p) { return p.dtype != F32 && fz::env_int("BTK_XB", 0) == 1; }
+// 16-bit dtypes run the batched pipeline (1.6x the cluster kernel on cfg5);
+// BTK_XB=0 selects the cluster kernel (development A/B)
+inline bool use_batched(const Problem& p) { return p.dtype != F32 && fz::env_int("BTK_XB", 1) != 0; }
 
 inline int xb_capc(const Problem& p, int ncand) {
   // expected keys per (owner, chunk): the kept fraction of the chunk over C
@@ -1183,12 +1265,12 @@ struct XBBufs {
   size_t spl, seg, cnt, total;
 };
 inline XBBufs xb_bufs(const Problem& p) {
-  const size_t br = (size_t)xb_rows(p.m);
+  const size_t br = (size_t)xb_rows_cap(p.m);
   const int ncand = (int)(p.b / XB_C * p.kb);
   XBBufs u{};
   u.spl = al256((size_t)p.m * (XB_C + 1) * 4);
-  u.seg = al256(br * XB_C * XB_C * (size_t)xb_capc(p, ncand) * 4);
-  u.cnt = al256(br * XB_C * (XB_C + 1) * 4);
+  u.seg = 2 * al256(br * XB_C * XB_C * (size_t)xb_capc(p, ncand) * 4);  // double-buffered
+  u.cnt = 2 * al256(br * XB_C * (XB_C + 1) * 4);
   u.total = u.spl + u.seg + u.cnt;
   return u;
 }
@@ -1202,6 +1284,8 @@ cudaError_t run_batched(const Problem& p, const XArgs& a, uint8_t* w, cudaStream
   A.spl = reinterpret_cast<uint32_t*>(w);
   A.seg = reinterpret_cast<uint32_t*>(w + u.spl);
   A.cnt = reinterpret_cast<uint32_t*>(w + u.spl + u.seg);
+  A.seg_elems = u.seg / 2 / 4;
+  A.cnt_elems = u.cnt / 2 / 4;
   switch (p.kb) {
     case 1: return xb_launch_all<DT, 1>(A, st);
     case 2: return xb_launch_all<DT, 2>(A, st);
@@ -1211,12 +1295,20 @@ cudaError_t run_batched(const Problem& p, const XArgs& a, uint8_t* w, cudaStream
 }
 }  // namespace xc
 
+int xchg_launch_count(const Problem& p) {
+  if (!xc::use_batched(p)) return 2;
+  const int64_t br = xc::xb_rows(p.m);
+  return (int)(2 + 2 * ((p.m + br - 1) / br));
+}
+
 size_t xchg_workspace_bytes(const Problem& p) {
   // fallback-row counter + list, one scratch slot (pool + k keys) per
   // fallback CTA, and the batched pipeline's per-batch buffers
   const int64_t P = p.b * p.kb;
   const int64_t ctas = std::min<int64_t>(p.m, xc::FB_CTAS);
-  const size_t xb = xc::use_batched(p) ? xc::xb_bufs(p).total : 0;
+  // (sized whenever the batched pipeline may run, so the choice can change
+  // between preparing a workspace and launching on it)
+  const size_t xb = p.dtype != F32 ? xc::xb_bufs(p).total : 0;
   return al256(4) + al256((size_t)p.m * 4) + al256((size_t)ctas * (P + p.k) * 8) + xb;
 }
 

@@ -66,14 +66,15 @@ _PLANS = [
     (128, 65536, 16384, 2048, 8, _lib.BTK_F32, 1, 1),
     (128, 1 << 20, 256, 512, 1, _lib.BTK_BF16, 1, 1),       # cfg3
     (4096, 32768, 512, 512, 1, _lib.BTK_BF16, 1, 1),        # cfg4: warp-per-row kernel
-    (8192, 1 << 20, 65536, 65536, 2, _lib.BTK_BF16, 1, 2),  # cfg5: cluster exchange + fallback kernel
+    # cfg5: batched exchange (split, 56 batches of 148 rows x (partition, sort), fallback kernel)
+    (8192, 1 << 20, 65536, 65536, 2, _lib.BTK_BF16, 1, 114),
 ]
 
 
 @pytest.mark.parametrize("plan", _PLANS, ids=lambda p: f"m{p[0]}-n{p[1]}-k{p[2]}-b{p[3]}-kb{p[4]}")
 def test_launch_planner_host_side(plan):
     """The host-side planner (no GPU needed) picks the fused single-launch
-    path for cfg1-4 and the cluster-exchange kernel (plus its row-masked
+    path for cfg1-4 and the exchange pipeline (batched partition + owner sorts, plus its
     fallback K2) for cfg5, and sizes the workspace for the path that runs."""
     m, n, k, b, kb, dt, fused, launches = plan
     lib = _lib.load()

@@ -1,8 +1,11 @@
-"""The cluster-exchange kernel (btk_xchg.cu, family BTK_FAM_XCHG) against
-the oracle: every 16-bit dtype and k_b it serves, thresholds inside and at
-the pool edge, tie-heavy rows that take its row-masked fallback next to
-rows that do not, subnormals / signed zeros, and the fp32 64-bit-key
-variant forced with BTK_XC=1.
+"""The exchange family (btk_xchg.cu, BTK_FAM_XCHG) against the oracle, both
+pipelines: the batched cluster-free one (16-bit default: xb_split /
+xb_part / xb_sort) and the 16-CTA cluster kernel (BTK_XB=0).  Every 16-bit
+dtype and k_b served, thresholds inside and at the pool edge, tie-heavy
+rows that take the fallback kernel next to rows that do not, subnormals /
+signed zeros, several batches (double-buffered, partition and sort on two
+streams, inside a CUDA graph), and the fp32 64-bit-key cluster variant
+forced with BTK_XC=1.
 
 Reference: approx.py:208-282 (stage1 + topk_with_indices),
 exact.py:130-159 (canonical order).
@@ -18,6 +21,15 @@ from oracle import bucketed_oracle as O
 from tests.special_inputs import TORCH, special, to_dtype
 
 pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(params=["batched", "cluster"])
+def pipe(request, monkeypatch):
+    if request.param == "cluster":
+        monkeypatch.setenv("BTK_XB", "0")
+    else:
+        monkeypatch.delenv("BTK_XB", raising=False)
+    return request.param
 
 _DTC = {"f32": _lib.BTK_F32, "bf16": _lib.BTK_BF16, "f16": _lib.BTK_F16}
 
@@ -65,7 +77,7 @@ SHAPES = [
 
 
 @pytest.mark.parametrize("dn", ["bf16", "f16"])
-def test_xchg_normal_and_ties(dn):
+def test_xchg_normal_and_ties(dn, pipe):
     rng = np.random.default_rng(11)
     for (m, n, k, b, kb) in SHAPES:
         assert _family(m, n, k, b, kb, dn) == _lib.BTK_FAM_XCHG, (m, n, k, b, kb)
@@ -76,7 +88,7 @@ def test_xchg_normal_and_ties(dn):
 
 
 @pytest.mark.parametrize("dn", ["bf16", "f16"])
-def test_xchg_special_values(dn):
+def test_xchg_special_values(dn, pipe):
     rng = np.random.default_rng(12)
     for (m, n, k, b, kb) in SHAPES[:4]:
         for kind in ("subnormal", "subnormal_ties", "pm0"):
@@ -84,7 +96,7 @@ def test_xchg_special_values(dn):
 
 
 @pytest.mark.parametrize("dn", ["bf16", "f16"])
-def test_xchg_fallback_rows_mixed(dn):
+def test_xchg_fallback_rows_mixed(dn, pipe):
     """Tie-heavy rows overflow an owner and go to the fallback kernel;
     normal rows in the same batch stay in-cluster; both are exact."""
     rng = np.random.default_rng(13)
@@ -97,9 +109,10 @@ def test_xchg_fallback_rows_mixed(dn):
     assert 0 not in rows and 2 not in rows and 1 in rows, rows
 
 
-def test_xchg_cfg5_rows_stay_in_cluster():
+def test_xchg_cfg5_rows_stay_in_cluster(pipe):
     """N(0,1) cfg5 rows: no fallback (the splitter margins hold)."""
-    x = torch.randn(32, 1 << 20, device="cuda").to(torch.bfloat16)
+    torch.manual_seed(5)
+    x = torch.randn(200 if pipe == "batched" else 32, 1 << 20, device="cuda").to(torch.bfloat16)
     rows, op = _fallback_rows(x, 65536, 65536, 2)
     assert rows == [], rows
     # and the outputs equal the chunked-pool path's on the same input
@@ -111,6 +124,23 @@ def test_xchg_cfg5_rows_stay_in_cluster():
         del os.environ["BTK_XC"]
     assert torch.equal(op.indices, ref.indices)
     assert torch.equal(op.values.view(torch.int16), ref.values.view(torch.int16))
+
+
+@pytest.mark.parametrize("streams", ["1", "0"])
+def test_xb_several_batches(monkeypatch, streams):
+    """Batches of 2 rows (BTK_XB_ROWS=2): double-buffered partition / sort
+    buffers, the sorts on the side stream (or all on one stream), a
+    tie-heavy fallback row in the middle batch."""
+    monkeypatch.setenv("BTK_XB_ROWS", "2")
+    monkeypatch.setenv("BTK_XB_STREAMS", streams)
+    rng = np.random.default_rng(15)
+    for dn in ("bf16", "f16"):
+        m, n, k, b, kb = 7, 262144, 20000, 16384, 2
+        x32 = torch.from_numpy(rng.standard_normal((m, n), dtype=np.float32)).to(TORCH[dn]).float().numpy()
+        x32[3] = 0.25
+        _check(x32, dn, k, b, kb)
+        rows, _ = _fallback_rows(to_dtype(x32, dn).cuda(), k, b, kb)
+        assert rows == [3], rows
 
 
 def test_xchg_fp32_forced(monkeypatch):
@@ -125,17 +155,23 @@ def test_xchg_fp32_forced(monkeypatch):
 
 
 @pytest.mark.parametrize("shape", [
-    (3, 65536, 64, 64, 1, torch.float32),          # fused_narrow (cluster, TMA ring)
-    (1200, 2048, 64, 64, 1, torch.bfloat16),       # fused_rows (one warp per row)
-    (2, 65536, 16384, 8192, 2, torch.float32),     # fused_wide
-    (2, 262144, 20000, 16384, 2, torch.bfloat16),  # fused_xchg
-], ids=["narrow", "rows", "wide", "xchg"])
-def test_inputs_ready_overlapped_launches_equal_serial(shape):
+    (3, 65536, 64, 64, 1, torch.float32, None),          # fused_narrow (cluster, TMA ring)
+    (1200, 2048, 64, 64, 1, torch.bfloat16, None),       # fused_rows (one warp per row)
+    (2, 65536, 16384, 8192, 2, torch.float32, None),     # fused_wide
+    (2, 262144, 20000, 16384, 2, torch.bfloat16, "0"),   # fused_xchg (cluster)
+    (2, 262144, 20000, 16384, 2, torch.bfloat16, None),  # batched exchange, one batch
+    (5, 262144, 20000, 16384, 2, torch.bfloat16, "2"),   # batched exchange, 3 batches, 2 streams
+], ids=["narrow", "rows", "wide", "xchg", "xb", "xb-batches"])
+def test_inputs_ready_overlapped_launches_equal_serial(shape, monkeypatch):
     """BTK_INPUT_READY launches back to back (eager and in a CUDA graph)
     over rotating buffers: every step's outputs equal the conservative
     launch's, and the last write wins (writes still wait for the
     predecessor)."""
-    m, n, k, b, kb, dt = shape
+    m, n, k, b, kb, dt, xb = shape
+    if xb == "0":
+        monkeypatch.setenv("BTK_XB", "0")
+    elif xb is not None:
+        monkeypatch.setenv("BTK_XB_ROWS", xb)
     xs = [torch.randn(m, n, device="cuda").to(dt) for _ in range(3)]
     sch = btk.BucketScheme(b, kb)
     ready = btk.ApproxTopK(m, n, k, sch, dtype=dt, device="cuda", inputs_ready=True)
