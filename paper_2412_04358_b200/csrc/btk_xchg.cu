@@ -628,7 +628,17 @@ __global__ void __launch_bounds__(XB_NT) xb_split(XBArgs A) {
     const uint8_t* colp = static_cast<const uint8_t*>(a.x) + (row * a.row_stride + col) * ESZ;
     Scanner<DT, KB> sc;
     sc.init();
-    for (int t = 0; t < a.s; ++t) sc.row(ldg_stream(colp + (int64_t)t * a.b * ESZ), t);
+    // 8 loads in flight per thread (one latency per 8 view-rows, not per row)
+    const uint32_t vs = (uint32_t)(a.b * ESZ);
+    int t0 = 0;
+    for (; t0 + 8 <= a.s; t0 += 8) {
+      uint4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = ldg_stream(colp + (uint32_t)(t0 + u) * vs);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) sc.row(v[u], t0 + u);
+    }
+    for (; t0 < a.s; ++t0) sc.row(ldg_stream(colp + (uint32_t)t0 * vs), t0);
     sc.each_comp((int)(col / V), a.b, 0, a.geo, [&](int64_t cc, int z, uint64_t comp) {
       smp[c][g * V * KB + (int)(cc - col) * KB + z] = comp;
     });

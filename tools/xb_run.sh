@@ -1,2 +1,3 @@
-timeout 600 python -m pytest tests/test_gpu_contig.py -q -x 2>&1 | tail -2
-for pf in 0 1 2; do for vpl in 16 32 64; do echo "pf=$pf vpl=$vpl"; BTK_CONTIG_PF=$pf BTK_CONTIG_VPL=$vpl bash tools/bench_sweep.sh cfg3c_r2; done; done
+timeout 600 python tools/xc_check.py 2>&1 | grep -v "^f32" | grep -v "True val True" | tail -5
+bash tools/bench_sweep.sh cfg5
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/xb_launch_1.csv python tools/xb_prof.py > /dev/null 2>&1
