@@ -620,11 +620,15 @@ __global__ void __launch_bounds__(XB_NT) xb_split(XBArgs A) {
   __shared__ unsigned long long est[C][C + 1];
   pdl_trigger();
   if (!a.early) pdl_wait();
-  const int span = a.cols / G;  // columns between sampled groups (multiple of V)
+  // sample sites of GS adjacent vector groups (64 contiguous bytes per
+  // view-row: whole DRAM bursts, not one 16-byte piece per burst), NS sites
+  // spread over the chunk at pseudo-random offsets
+  constexpr int GS = G < 4 ? G : 4, NS = G / GS;
+  const int span = a.cols / NS;  // columns between sites (multiple of GS * V)
   if (tid < C * G) {
-    const int c = tid / G, g = tid % G;
-    const int off = (int)(((uint64_t)row * 40503u + c * 977u + g * 7u) % (uint64_t)(span / V)) * V;
-    const int64_t col = (int64_t)c * a.cols + (int64_t)g * span + off;
+    const int c = tid / G, g = tid % G, site = g / GS, w = g % GS;
+    const int off = (int)(((uint64_t)row * 40503u + c * 977u + site * 7u) % (uint64_t)(span / (GS * V))) * (GS * V);
+    const int64_t col = (int64_t)c * a.cols + (int64_t)site * span + off + w * V;
     const uint8_t* colp = static_cast<const uint8_t*>(a.x) + (row * a.row_stride + col) * ESZ;
     Scanner<DT, KB> sc;
     sc.init();

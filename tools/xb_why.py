@@ -24,10 +24,10 @@ r = SPC * q + 4 * math.sqrt(SPC * q * (1 - q) / C) + 0.5
 rthr = SPC if q >= 1 else min(SPC, math.ceil(r))
 ncand = b // C * kb
 capc = min((int(2.0 * (rthr / SPC * ncand / C)) + 128 + 31) & ~31, 8192)
-br = min(m, int(os.environ.get("BTK_XB_ROWS", "64")))
+br = min(m, 148)  # workspace is sized for the row cap; one batch when BTK_XB_ROWS >= m
 off = al(4) + al(m * 4) + al(min(m, 148) * (P + k) * 8)
 spl = ws[off:off + m * 17 * 4].view(torch.int32).cpu().numpy().reshape(m, 17).view(np.uint32)
-off += al(m * 17 * 4) + al(br * C * C * capc * 4)
+off += al(m * 17 * 4) + 2 * al(br * C * C * capc * 4)  # double-buffered sub-slots
 cn = ws[off:off + br * C * 17 * 4].view(torch.int32).cpu().numpy().reshape(br, C, 17).view(np.uint32)
 print("rthr", rthr, "capc", capc, "br", br)
 for rr in rows[:6]:
