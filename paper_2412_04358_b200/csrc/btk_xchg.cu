@@ -723,7 +723,9 @@ __device__ __forceinline__ void xb_each_rec(const Scanner<DT, KB>& sc, int g, co
   }
 }
 
-template <int DT, int KB>
+// ST (s <= 16 view-rows): the view-row takes 4 record bits, so the owner
+// fits in the record too and is not looked up a second time
+template <int DT, int KB, bool ST>
 __global__ void __launch_bounds__(XB_NT, 2) xb_part(XBArgs A) {
   constexpr int V = Vec<DT>::V;
   constexpr int ESZ = VT<DT>::W / 8;
@@ -822,7 +824,7 @@ __global__ void __launch_bounds__(XB_NT, 2) xb_part(XBArgs A) {
     // bits 11..15 of its record (view-rows < 1024); the owner is looked up
     // again after the scan (no second per-item register array).
     auto owner = [&](uint32_t r, bool ok) -> uint32_t {
-      const uint32_t vk = ((r >> 16) << tb) | (tmax - (((r >> 1) & 0x3FFu) >> tsh));  // fine key
+      const uint32_t vk = ((r >> 16) << tb) | (tmax - (((r >> 1) & (ST ? 15u : 0x3FFu)) >> tsh));  // fine key
       const uint32_t off = vk - vthr;  // wraps below the threshold
       uint32_t d = vk < vthr ? (uint32_t)C : 0u;
       if (off < (uint32_t)LUTN) d = lut[off];
@@ -834,7 +836,12 @@ __global__ void __launch_bounds__(XB_NT, 2) xb_part(XBArgs A) {
 #pragma unroll
     for (int i = 0; i < IT; ++i) {
       const uint32_t d = owner(rec[i], act);
-      if (d < (uint32_t)C) rec[i] |= lsd::count_digit<NT>(cnt, d) << 11;
+      if constexpr (ST) {  // vkey << 16 | owner << 10 | rank << 5 | view-row << 1 | negzero
+        rec[i] |= d << 10;
+        if (d < (uint32_t)C) rec[i] |= lsd::count_digit<NT>(cnt, d) << 5;
+      } else {
+        if (d < (uint32_t)C) rec[i] |= lsd::count_digit<NT>(cnt, d) << 11;
+      }
     }
     lsd::digit_scan_from<NT, 8>(cnt, ws, sendcnt, dex, run);
     // key = (vkey - spl[d+1]) << ib1 | (imax - idx) << 1 | negzero with
@@ -842,11 +849,12 @@ __global__ void __launch_bounds__(XB_NT, 2) xb_part(XBArgs A) {
     const uint32_t kb0 = 2u * (a.geo.imax - (uint32_t)(col0 + (int64_t)g * V));
 #pragma unroll
     for (int i = 0; i < IT; ++i) {
-      const uint32_t d = owner(rec[i], act);
+      const uint32_t d = ST ? (rec[i] >> 10) & 31u : owner(rec[i], act);
       const uint32_t dd = d < (uint32_t)C ? d : 0u;  // in-range reads for unselected items
-      const uint32_t pos = lsd::digit_base<NT>(cnt, dd) + ((rec[i] >> 11) & 31u);
-      const uint32_t key = ((rec[i] >> 16) << ib1) - kofs[dd] + kb0 - 2u * (uint32_t)(i / KB) -
-                           (((rec[i] >> 1) & 0x3FFu) << lb1) + (rec[i] & 1u);
+      const uint32_t pos = lsd::digit_base<NT>(cnt, dd) + (ST ? (rec[i] >> 5) & 31u : (rec[i] >> 11) & 31u);
+      const uint32_t t = ST ? (rec[i] >> 1) & 15u : (rec[i] >> 1) & 0x3FFu;
+      const uint32_t key = ((rec[i] >> 16) << ib1) - kofs[dd] + kb0 - 2u * (uint32_t)(i / KB) - (t << lb1) +
+                           (rec[i] & 1u);
       if (d < (uint32_t)C && pos < capc) seg[dd * ostride + pos] = key;
     }
     __syncthreads();
@@ -1036,7 +1044,10 @@ cudaError_t xb_attrs() {
   cudaError_t e = cudaFuncSetAttribute((const void*)xb_sort<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)XB_SORT_SMEM);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute((const void*)xb_part<DT, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  e = cudaFuncSetAttribute((const void*)xb_part<DT, KB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)XB_PART_SMEM);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute((const void*)xb_part<DT, KB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)XB_PART_SMEM);
   if (e != cudaSuccess) return e;
   attr_done = dev;
@@ -1112,7 +1123,8 @@ cudaError_t xb_launch_all(XBArgs A, cudaStream_t st) {
       e = cudaStreamWaitEvent(st, sd->sort[buf], 0);  // sort i-2 released this buffer
       if (e != cudaSuccess) return e;
     }
-    e = cudaLaunchKernelEx(&cfg, xb_part<DT, KB>, A);
+    e = A.x.s <= 16 ? cudaLaunchKernelEx(&cfg, xb_part<DT, KB, true>, A)
+                    : cudaLaunchKernelEx(&cfg, xb_part<DT, KB, false>, A);
     if (e != cudaSuccess) return e;
     cfg.dynamicSmemBytes = XB_SORT_SMEM;
     cfg.blockDim = dim3(XB_SNT);
