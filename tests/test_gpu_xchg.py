@@ -198,3 +198,36 @@ def test_inputs_ready_overlapped_launches_equal_serial(shape, monkeypatch):
         g.replay()
     torch.cuda.synchronize()
     assert torch.equal(ready.indices, want[4 % 3][1]) and torch.equal(ready.values, want[4 % 3][0])
+
+
+def _xchg_shapes(seed, count):
+    """Seeded shapes the exchange family serves: s below / above 16 and not a
+    multiple of the load batch, thresholds from a handful of keys to the
+    whole pool, k_b 1/2/4, batches that do not divide m."""
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < count:
+        b = int(rng.choice([4096, 8192, 16384, 32768, 65536]))
+        kb = int(rng.choice([1, 2, 4]))
+        s = int(rng.choice([1, 2, 3, 5, 7, 8, 9, 13, 16, 17, 24, 31]))
+        P = b * kb
+        if P <= 16384 or s < kb or b // 16 * kb > 8192:
+            continue
+        k = int(min(P, 16 * 4096, max(1, rng.integers(1, P + 1) if rng.random() < 0.7 else P)))
+        m = int(rng.integers(1, 6))
+        out.append((m, s * b, k, b, kb))
+    return out
+
+
+@pytest.mark.parametrize("dn", ["bf16", "f16"])
+def test_xb_random_shapes(dn, monkeypatch):
+    """Randomised exchange-family shapes through the batched pipeline
+    (several batch sizes) against the oracle, normal and tie-heavy rows."""
+    rng = np.random.default_rng(21 if dn == "bf16" else 22)
+    for i, (m, n, k, b, kb) in enumerate(_xchg_shapes(31 if dn == "bf16" else 32, 10)):
+        assert _family(m, n, k, b, kb, dn) == _lib.BTK_FAM_XCHG, (m, n, k, b, kb)
+        monkeypatch.setenv("BTK_XB_ROWS", str(1 + i % 3))
+        x32 = torch.from_numpy(rng.standard_normal((m, n), dtype=np.float32)).to(TORCH[dn]).float().numpy()
+        if i % 2:
+            x32 = np.round(x32 * 8) / 8
+        _check(x32, dn, k, b, kb)
