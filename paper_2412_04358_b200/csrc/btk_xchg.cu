@@ -554,32 +554,37 @@ cudaError_t launch_fallback(const XArgs& a, int64_t kb, uint64_t* slots, int64_t
 }
 
 // ================================================================ batched pipeline
-// The same algorithm without clusters, for 16-bit dtypes: the splitters come
-// from a sampling pass, so the chunks of a row never synchronise with each
-// other — no cluster barriers, and the owner sorts run as independent,
-// fully occupied CTAs.  Intermediates of a batch of rows stay in L2.
+// The same algorithm without clusters, for 16-bit dtypes (the default for
+// them; BTK_XB=0 selects the cluster kernel above).  The splitters come from
+// a sampling pass, so the chunks of a row never synchronise with each other:
+// no cluster barriers, and the owner sorts run as independent, fully
+// occupied CTAs.  Rows go in batches of up to 148; a batch's partition and
+// sort are two launches, the sorts on a side stream over double-buffered
+// sub-slots so batch i's sort can overlap batch i+1's partition.
 //
-//   xb_split   one CTA per row (all rows, once): Stage 1 of SPC/(V*KB)
-//              sampled column groups per chunk (~3% of the row) gives SPC
-//              sampled candidates per chunk; local quantiles at the owner
-//              boundaries and at the threshold rank, averaged over the C
-//              chunks and rounded down to whole values -> C splitter vkeys.
+//   xb_split   one CTA per row (all rows, once): Stage 1 of sample sites of
+//              64 contiguous bytes per view-row (~1.6% of the row) gives SPC
+//              sampled candidates per chunk of b/C columns; local quantiles
+//              at the owner boundaries (fractional ranks, interpolated) and
+//              at the threshold rank, averaged over the C chunks and rounded
+//              down to fine keys (vkey << TB | top TB bits of the complemented
+//              view-row; TB as large as keeps the owner table <= LUTN).
 //   xb_part    grid (C, BR) per batch: CTA (c, r) runs Stage 1 on chunk c of
-//              row r in shared memory, assigns each candidate its owner
-//              (keys >= spl[1]: owner 0; else a table lookup on the vkey;
+//              row r with the candidates in registers, assigns each its
+//              owner (fine keys >= spl[1]: owner 0; else a table lookup;
 //              below the threshold: none) and scatters the 32-bit sort keys
-//              into its own sub-slot of each owner's segment, stably (bucket
-//              order), with the per-owner counts and the chunk's max vkey.
+//              into its own sub-slot of each owner, stably (bucket order),
+//              with the per-owner counts and the chunk's max vkey.
 //   xb_sort    grid (C, BR) per batch: owner d of row r reads the C x (C+1)
 //              counts, derives the row's verdict and its output offset (the
 //              same in every CTA of the row), gathers its C sub-slots in
-//              chunk order, sorts them (4-bit LSD over the bits above the
-//              bucket id) and emits.  Rows whose verdict fails (sub-slot or
-//              owner overflow, key range, fewer than k kept) go to the
-//              fallback list, finished by xc_fallback after the last batch.
+//              chunk order into registers, sorts them (4-bit LSD over the
+//              bits above the bucket id) and emits.  Rows whose verdict fails
+//              (sub-slot or owner overflow, key range, fewer than k kept) go
+//              to the fallback list, finished by xc_fallback after the last
+//              batch.
 constexpr int XB_C = 16;       // chunks (= owners) per row
 constexpr int XB_NT = 512;     // threads of every xb CTA
-constexpr int XB_IPT = 16;     // candidates per thread in xb_part (ncand <= 8192)
 constexpr int XB_CAP = 8192;   // keys per owner in xb_sort (SNT x ITEMS)
 constexpr int XB_SNT = 512;    // threads of an owner sort (256 x 32 items: fewer scan
                                // instructions but 80 registers, lower occupancy: slower)
