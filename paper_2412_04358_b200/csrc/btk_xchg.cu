@@ -1,6 +1,15 @@
-// Cluster-exchange fused kernel ("xchg"): Stage 1 + Stage 2 of one row in
-// ONE launch for large pools (cfg5: 131072 survivors per row, k = 65536;
-// cfg2: 16384 survivors = k), with no HBM round trip for the candidates.
+// The exchange family for large pools (cfg5: 131072 survivors per row,
+// k = 65536): Stage 1 + Stage 2 partitioned by value range over 16 owners
+// per row, with no radix passes over the whole pool.  Two pipelines:
+//
+//   * the batched pipeline (xb_split / xb_part / xb_sort, below the cluster
+//     kernel; the default for 16-bit dtypes): the same five steps as
+//     ordinary launches over batches of rows, splitters from a sampling
+//     pass, intermediates in global memory (~0.3 MB of keys per row);
+//   * the cluster kernel (fused_xchg; BTK_XB=0, and fp32 with BTK_XC=1),
+//     described here: one row per 16-CTA cluster in ONE launch, with no HBM
+//     round trip for the candidates.  Its cluster barriers left ~70% of
+//     each CTA's life waiting, hence the batched pipeline.
 //
 // Restates reference approx.py:208-282 (stage1 + topk_with_indices) and
 // exact.py:130-159 (_canonical_order) for the B200: a cluster of C CTAs
