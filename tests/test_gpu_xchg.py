@@ -11,6 +11,8 @@ Reference: approx.py:208-282 (stage1 + topk_with_indices),
 exact.py:130-159 (canonical order).
 """
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -231,3 +233,32 @@ def test_xb_random_shapes(dn, monkeypatch):
         if i % 2:
             x32 = np.round(x32 * 8) / 8
         _check(x32, dn, k, b, kb)
+
+
+def test_xb_first_call_inside_graph_capture(tmp_path):
+    """A fresh process whose first exchange call (several batches: the side
+    stream and its events are created lazily) happens inside CUDA graph
+    capture: capture succeeds and the replay equals an eager call."""
+    import subprocess
+    import sys
+    script = tmp_path / "cap.py"
+    script.write_text(
+        "import os, sys, torch\n"
+        "sys.path.insert(0, os.getcwd())\n"
+        "os.environ['BTK_XB_ROWS'] = '2'\n"
+        "import paper_2412_04358_b200 as btk\n"
+        "x = torch.randn(5, 262144, device='cuda').to(torch.bfloat16)\n"
+        "op = btk.ApproxTopK(5, 262144, 20000, btk.BucketScheme(16384, 2), dtype=torch.bfloat16, device='cuda')\n"
+        "s = torch.cuda.Stream()\n"
+        "g = torch.cuda.CUDAGraph()\n"
+        "with torch.cuda.stream(s):\n"
+        "    with torch.cuda.graph(g, stream=s):\n"
+        "        op.launch(x)\n"
+        "g.replay()\n"
+        "torch.cuda.synchronize()\n"
+        "r = btk.approx_topk(x, 20000, btk.BucketScheme(16384, 2))\n"
+        "assert torch.equal(op.indices, r.indices) and torch.equal(op.values, r.values)\n"
+        "print('ok')\n")
+    out = subprocess.run([sys.executable, str(script)], capture_output=True, text=True, timeout=300,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
