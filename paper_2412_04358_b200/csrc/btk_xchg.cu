@@ -900,7 +900,7 @@ __global__ void __launch_bounds__(XB_SNT, XB_SMIN) xb_sort(XBArgs A) {
   __shared__ uint32_t cn[C][C + 1];
   __shared__ uint32_t lspl[C + 1];
   __shared__ uint32_t tot[C], pre[C + 1];
-  __shared__ uint32_t s_vary, s_and, s_mx;
+  __shared__ uint32_t s_vary, s_and;
   __shared__ int s_why;
   __shared__ uint32_t s_start;
   pdl_trigger();
@@ -909,38 +909,51 @@ __global__ void __launch_bounds__(XB_SNT, XB_SMIN) xb_sort(XBArgs A) {
   if (tid <= C) lspl[tid] = A.spl[row * (C + 1) + tid];
   if (tid == 0) { s_vary = 0u; s_and = ~0u; }
   __syncthreads();
-  if (tid < C) {
-    uint32_t t = 0;
-    for (int c = 0; c < C; ++c) t += cn[c][tid];
-    tot[tid] = t;
-  } else if (tid == C) {
-    uint32_t m = 0;
-    for (int c = 0; c < C; ++c) m = max(m, cn[c][C]);
-    s_mx = m;
-  }
-  const int over = __syncthreads_or(tid < C * C && cn[tid / C][tid % C] > (uint32_t)A.capc);
-  if (tid == 0) {  // verdict (identical in every CTA of the row) and offsets
-    int why = over ? 1 : 0;
-    uint32_t sum = 0;
+  if (tid < 32) {  // verdict and offsets, one warp (identical in every CTA of the row)
+    const int q = lane;  // lanes < C: owner q (totals, checks); chunk q (this owner's prefix)
+    uint32_t t = 0, over = 0;
+    if (q < C) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const uint32_t v = cn[c][q];
+        t += v;
+        over |= v > (uint32_t)A.capc ? 1u : 0u;  // a sub-slot overflowed
+      }
+    }
+    const uint32_t mx = __reduce_max_sync(0xFFFFFFFFu, q < C ? cn[q][C] : 0u);  // the row's max vkey
+    uint32_t inc = t;  // inclusive prefix of the owner totals
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+      if (lane >= o) inc += v;
+    }
+    const uint32_t sum = __shfl_sync(0xFFFFFFFFu, inc, C - 1);
     const int tb = (int)lspl[0];
-    for (int q = 0; q < C; ++q) {
-      if (q == d) s_start = sum;
-      sum += tot[q];
-      if (tot[q] > (uint32_t)XB_CAP) why |= 1;
+    uint32_t why = over;
+    if (q < C) {
+      if (t > (uint32_t)XB_CAP) why |= 1u;
       // the owner's value offsets must fit the 32-bit key above the index field
-      const uint32_t hi = q == 0 ? s_mx : (lspl[q] - 1u) >> tb;
-      if (tot[q] && ((uint64_t)(hi - (lspl[q + 1] >> tb)) >> (32 - ib1)) != 0ull) why |= 2;
+      const uint32_t hi = q == 0 ? mx : (lspl[q] - 1u) >> tb;
+      if (t && ((uint64_t)(hi - (lspl[q + 1] >> tb)) >> (32 - ib1)) != 0ull) why |= 2u;
+      tot[q] = t;
     }
-    if (lspl[1] - lspl[C] > (uint32_t)LUTN) why |= 2;
-    if (sum < (uint64_t)a.k) why |= 4;
-    if (why && d == 0) a.fb_list[atomicAdd(a.fb_count, 1)] = (int)row;
-    s_why = why;
-    uint32_t p = 0;
-    for (int c = 0; c < C; ++c) {
-      pre[c] = p;
-      p += cn[c][d];
+    why = __reduce_or_sync(0xFFFFFFFFu, why);
+    if (lspl[1] - lspl[C] > (uint32_t)LUTN) why |= 2u;
+    if (sum < (uint64_t)a.k) why |= 4u;
+    // this owner's sub-slot prefix over the chunks (lane = chunk)
+    const uint32_t v = q < C ? cn[q][d] : 0u;
+    uint32_t pinc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t w = __shfl_up_sync(0xFFFFFFFFu, pinc, o);
+      if (lane >= o) pinc += w;
     }
-    pre[C] = p;
+    if (q <= C) pre[q] = pinc - v;  // lane C: the owner's total
+    if (q == d) s_start = inc - t;
+    if (lane == 0) {
+      s_why = (int)why;
+      if (why && d == 0) a.fb_list[atomicAdd(a.fb_count, 1)] = (int)row;
+    }
   }
   __syncthreads();
   const int R = (int)tot[d];
@@ -958,13 +971,23 @@ __global__ void __launch_bounds__(XB_SNT, XB_SMIN) xb_sort(XBArgs A) {
     for (int st = C / 2; st > 0; st >>= 1)
       if (pre[cc + st] <= (uint32_t)p0) cc += st;
     KT kor = 0, kand = ~(KT)0;
+    // addresses first (shared-memory walk over the chunk prefixes), then
+    // every load at once: one global latency per thread, not one per key
+    uint32_t off[ITEMS];
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
-      key[i] = 0;  // pads sort last
       const int p = p0 + i;
+      off[i] = 0xFFFFFFFFu;
       if (i < items && p < R) {
         while (pre[cc + 1] <= (uint32_t)p) ++cc;
-        key[i] = seg[(int64_t)cc * A.capc + (p - (int)pre[cc])];
+        off[i] = (uint32_t)cc * (uint32_t)A.capc + (uint32_t)(p - (int)pre[cc]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) key[i] = off[i] != 0xFFFFFFFFu ? seg[off[i]] : (KT)0;  // pads (0) sort last
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      if (off[i] != 0xFFFFFFFFu) {
         kor |= key[i];
         kand &= key[i];
       }

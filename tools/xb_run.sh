@@ -1,2 +1,4 @@
-for mb in 2 3 4; do cp tmp_rows/libbtk$mb.so paper_2412_04358_b200/libbtk.so; echo "MINB=$mb"; bash tools/bench_sweep.sh cfg4; done
-cp tmp_rows/libbtk2.so paper_2412_04358_b200/libbtk.so
+timeout 600 python tools/xc_check.py 2>&1 | grep -v "^f32" | grep -v "True val True" | tail -3
+timeout 600 python -m pytest tests/test_gpu_xchg.py -q -x 2>&1 | tail -2
+bash tools/bench_sweep.sh cfg5
+ncu --metrics gpu__time_duration.sum --clock-control none --csv -k regex:xb_ --log-file gpurun_out/xb_l.csv python tools/xb_prof.py > /dev/null 2>&1
