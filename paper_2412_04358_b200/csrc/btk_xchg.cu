@@ -1054,10 +1054,14 @@ __global__ void __launch_bounds__(XB_SNT, XB_SMIN) xb_sort(XBArgs A) {
   const KT* src = buf;
   const int keep = (int)min((int64_t)R, a.k - start);
   const uint32_t vbase = lspl[d + 1] >> (int)lspl[0];
+  // 32-bit decode (16-bit dtypes, index field <= 26 bits): value bits from
+  // the owner's base vkey plus the key's offset, index = imax - field
+  const int64_t obase = row * a.k + start;
   for (int q = tid; q < keep; q += NT) {
     const KT key = src[padk<KT>(q)];
-    const uint64_t cc = ((uint64_t)(vbase + (key >> ib1)) << ib1) | (uint64_t)(key & ((1u << ib1) - 1u));
-    emit_comp<DT>(cc, row * a.k + start + q, a.geo, a.out_vals, a.out_idx);
+    const uint32_t vk = vbase + (key >> ib1);
+    store_bits<DT>(a.out_vals, obase + q, bits_of_key<DT>(vk, key & 1u));
+    a.out_idx[obase + q] = (int64_t)(a.geo.imax - ((key >> 1) & a.geo.imax));
   }
 }
 
