@@ -143,11 +143,12 @@ class ApproxTopK:
         if x.data_ptr() % 16:
             raise ValueError("prepared ApproxTopK needs a 16-byte aligned input (use approx_topk "
                              "for arbitrary views)")
-        st = self.lib.btk_approx_topk_flags(
-            x.data_ptr(), self.row_stride, self.dt, self.m, self.n, self.k, self.scheme.b,
-            self.scheme.k_b, self.layout, self.values.data_ptr(), self.indices.data_ptr(),
-            self.ws.data_ptr(), self.ws_bytes, self.flag.data_ptr(), self.launch_flags,
-            _ops.stream_handle(self.device) if stream is None else stream)
+        with torch.cuda.device(self.device):  # launches (and the exchange's side stream) on the op's GPU
+            st = self.lib.btk_approx_topk_flags(
+                x.data_ptr(), self.row_stride, self.dt, self.m, self.n, self.k, self.scheme.b,
+                self.scheme.k_b, self.layout, self.values.data_ptr(), self.indices.data_ptr(),
+                self.ws.data_ptr(), self.ws_bytes, self.flag.data_ptr(), self.launch_flags,
+                _ops.stream_handle(self.device) if stream is None else stream)
         _ops.raise_status(st, "(approx_topk)")
 
     def __call__(self, x: torch.Tensor) -> TopKResult:
