@@ -1,1 +1,4 @@
-for ns in 2 3 4 6; do for ev in 1 0; do echo "NS=$ns EVF=$ev"; BTK_CONTIG_NS=$ns BTK_CONTIG_EVF=$ev bash tools/bench_sweep.sh cfg3c_r2; done; done
+timeout 600 python tools/xc_check.py 2>&1 | grep -v "^f32" | grep -v "True val True" | tail -3
+timeout 600 python -m pytest tests/test_gpu_xchg.py -q -x 2>&1 | tail -2
+bash tools/bench_sweep.sh cfg5
+ncu --metrics gpu__time_duration.sum --clock-control none --csv -k regex:xb_ --log-file gpurun_out/xb_l.csv python tools/xb_prof.py > /dev/null 2>&1
