@@ -232,6 +232,8 @@ def test_xb_random_shapes(dn, monkeypatch):
         x32 = torch.from_numpy(rng.standard_normal((m, n), dtype=np.float32)).to(TORCH[dn]).float().numpy()
         if i % 2:
             x32 = np.round(x32 * 8) / 8
+        if i % 3 == 2:  # a sorted row: each owner's keys sit in a few chunks (sub-slot overflow)
+            x32[0] = np.sort(x32[0])
         _check(x32, dn, k, b, kb)
 
 
