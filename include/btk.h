@@ -154,7 +154,8 @@ enum btk_family {
                               scores (nothing materialised; name kept for ABI stability) + K2 */
   BTK_FAM_F64 = 6,         /* float64: 128-bit keys (btk_f64.cu) */
   BTK_FAM_POOL_CHUNKED = 7, /* s1_vec pool + histogram-chunked Stage 2 (btk_pool.cu) */
-  BTK_FAM_XCHG = 8,         /* fused_xchg: cluster per row, DSMEM value-range exchange (btk_xchg.cu) */
+  BTK_FAM_XCHG = 8,         /* value-range exchange (btk_xchg.cu): batched split / partition / owner-sort
+                               launches (16-bit default), or fused_xchg, a DSMEM cluster per row */
   BTK_FAM_CONTIG = 9        /* s1_contig (contiguous layout, warp per bucket, 128-bit loads) + K2 */
 };
 int btk_kernel_family(int64_t m, int64_t n, int64_t k, int64_t b, int64_t kb, int dtype,
