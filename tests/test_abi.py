@@ -90,6 +90,24 @@ def test_launch_planner_host_side(plan):
     assert lib.btk_uses_fused_path(m, n, k, b, kb, dt, _lib.BTK_INTERLEAVED, n + 1) == 0
 
 
+@pytest.mark.parametrize("m,launches", [(1, 4), (148, 4), (149, 6), (300, 8), (8192, 114)])
+def test_exchange_launch_count_per_batch(m, launches, monkeypatch):
+    """The batched exchange: split + (partition, sort) per batch of <= 148
+    rows + the fallback kernel; BTK_XB=0 (cluster kernel): 2 launches; the
+    workspace is sized for the row cap whatever BTK_XB_ROWS says."""
+    lib = _lib.load()
+    args = (m, 1 << 20, 65536, 65536, 2, _lib.BTK_BF16, _lib.BTK_INTERLEAVED, 1 << 20)
+    assert lib.btk_launch_count(*args) == launches
+    ws = lib.btk_plan_workspace_bytes(256, 1 << 20, _lib.BTK_BF16, m, 1 << 20, 65536, 65536, 2,
+                                      _lib.BTK_INTERLEAVED)
+    monkeypatch.setenv("BTK_XB_ROWS", "2")
+    assert lib.btk_plan_workspace_bytes(256, 1 << 20, _lib.BTK_BF16, m, 1 << 20, 65536, 65536, 2,
+                                        _lib.BTK_INTERLEAVED) == ws
+    assert lib.btk_launch_count(*args) == 2 + 2 * -(-m // 2)
+    monkeypatch.setenv("BTK_XB", "0")
+    assert lib.btk_launch_count(*args) == 2
+
+
 @pytest.mark.parametrize("s", ["1", "2", "4", "8"])
 def test_planner_cluster_overrides_stay_valid(s, monkeypatch):
     monkeypatch.setenv("BTK_S", s)

@@ -21,7 +21,7 @@ fams = {}
 while time.time() - t0 < budget:
     dn = str(rng.choice(["f32", "bf16", "f16"]))
     asg = btk.Assignment.INTERLEAVED if rng.random() < 0.75 else btk.Assignment.CONTIGUOUS
-    m = int(rng.choice([1, 2, 3, 5, 17, 300]))
+    m = int(rng.choice([1, 2, 3, 5, 17, 300, 1300]))
     if rng.random() < 0.5:  # power-of-two-ish large shapes (fused / exchange families)
         b = int(2 ** rng.integers(3, 17))
         s = int(rng.choice([1, 2, 3, 4, 7, 8, 16, 33]))
