@@ -1,5 +1,6 @@
-"""Quick GPU parity sweep of the cluster-exchange path (fused_xchg) against
-the oracle, every dtype / k_b / input kind (development tool)."""
+"""Quick GPU parity sweep of the exchange family against the oracle, every
+dtype / k_b / input kind (development tool): the batched pipeline by
+default, the cluster kernel with BTK_XB=0, fp32 through it with BTK_XC=1."""
 import os
 import sys
 import time

@@ -1,4 +1,6 @@
-"""Fallback-row census of fused_xchg (rowmask reasons; development tool)."""
+"""Fallback-row census of the cluster kernel fused_xchg (run with BTK_XB=0;
+rowmask reasons; development tool).  tools/xb_why.py is the batched
+pipeline's counterpart."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
