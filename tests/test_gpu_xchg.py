@@ -158,12 +158,14 @@ def test_xchg_fp32_forced(monkeypatch):
 
 @pytest.mark.parametrize("shape", [
     (3, 65536, 64, 64, 1, torch.float32, None),          # fused_narrow (cluster, TMA ring)
+    (128, 65536, 64, 64, 1, torch.float32, None),        # fused_narrow, one CTA per row when ready (cfg1)
+    (128, 1 << 20, 256, 512, 2, torch.bfloat16, None),   # fused_narrow, deep rows (cfg3), 32 KB stages when ready
     (1200, 2048, 64, 64, 1, torch.bfloat16, None),       # fused_rows (one warp per row)
     (2, 65536, 16384, 8192, 2, torch.float32, None),     # fused_wide
     (2, 262144, 20000, 16384, 2, torch.bfloat16, "0"),   # fused_xchg (cluster)
     (2, 262144, 20000, 16384, 2, torch.bfloat16, None),  # batched exchange, one batch
     (5, 262144, 20000, 16384, 2, torch.bfloat16, "2"),   # batched exchange, 3 batches, 2 streams
-], ids=["narrow", "rows", "wide", "xchg", "xb", "xb-batches"])
+], ids=["narrow", "narrow-solo", "narrow-deep", "rows", "wide", "xchg", "xb", "xb-batches"])
 def test_inputs_ready_overlapped_launches_equal_serial(shape, monkeypatch):
     """BTK_INPUT_READY launches back to back (eager and in a CUDA graph)
     over rotating buffers: every step's outputs equal the conservative
