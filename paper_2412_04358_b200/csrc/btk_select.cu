@@ -31,6 +31,9 @@ __global__ void __launch_bounds__(NT) k2_small(const uint64_t* __restrict__ in, 
                                                CompGeo g, int lognb, const int* mask,
                                                int64_t mask_stride) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
+  // let a programmatic dependent (the next call's Stage 1 with
+  // BTK_INPUT_READY) start streaming; it waits before its first write
+  asm volatile("griddepcontrol.launch_dependents;");
   uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw);
   uint8_t* aux = smem_raw + ((size_t)L * 8 + 127) / 128 * 128;
   const RankSmem S = rank_smem(sk, aux, L, kk, lognb, NT);

@@ -103,12 +103,16 @@ __global__ void s1_emit(Problem p, const uint64_t* __restrict__ pool, int64_t C,
 // k_b rounds of a warp max over composite keys (unique, canonical order).
 // Slices that do not start/end on a 16-byte boundary take scalar loads.
 template <int DT, int KB, int U>
-__global__ void __launch_bounds__(256, (U <= 4 ? 4 : 2)) s1_contig(Problem p, uint64_t* __restrict__ pool, int G) {
+__global__ void __launch_bounds__(256, (U <= 4 ? 4 : 2)) s1_contig(Problem p, uint64_t* __restrict__ pool, int G, int early) {
   constexpr int V = 16 / (VT<DT>::W / 8);
   constexpr int ESZ = VT<DT>::W / 8;
   const int lane = threadIdx.x & 31, gl = lane % G, per_warp = 32 / G;
   const int64_t P = p.b * p.kb;
   const int64_t tasks = p.m * p.b;
+  // programmatic dependent launch: with BTK_INPUT_READY the slices are
+  // streamed while the previous launch drains; the first pool write waits
+  fz::pdl_trigger();
+  if (!early) fz::pdl_wait();
   uint32_t bad = 0;
   // uniform buckets (b | n) and < 2^32 tasks: 32-bit index math, no 64-bit
   // divisions per bucket (they cost more than a bucket's loads)
@@ -193,6 +197,7 @@ __global__ void __launch_bounds__(256, (U <= 4 ? 4 : 2)) s1_contig(Problem p, ui
         top = other > top ? other : top;
       }
       if (top != 0ull && mine == top) ++head;  // comps are unique: one owner
+      if (early && z == 0) fz::pdl_wait();  // the previous launch may still read the pool
       if (gl == 0 && task < tasks && z < p.kb) pool[row * P + j * p.kb + z] = top;
     }
   }
@@ -211,9 +216,18 @@ static cudaError_t launch_contig(const Problem& p, uint64_t* pool, cudaStream_t 
   while (G < 32 && nv / (2 * G) >= vpl) G *= 2;
   const int64_t blocks = (p.m * p.b + 8 * (32 / G) - 1) / (8 * (32 / G));
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 16));
-  if (fz::env_int("BTK_CONTIG_U", 4) == 8) s1_contig<DT, KB, 8><<<grid, 256, 0, st>>>(p, pool, G);
-  else s1_contig<DT, KB, 4><<<grid, 256, 0, st>>>(p, pool, G);
-  return cudaGetLastError();
+  const int early = (p.flags & 1u) && fz::pdl_enabled() ? 1 : 0;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = fz::pdl_enabled() ? 1 : 0;
+  if (fz::env_int("BTK_CONTIG_U", 4) == 8) return cudaLaunchKernelEx(&cfg, s1_contig<DT, KB, 8>, p, pool, G, early);
+  return cudaLaunchKernelEx(&cfg, s1_contig<DT, KB, 4>, p, pool, G, early);
 }
 
 template <int DT>
