@@ -51,7 +51,16 @@ while time.time() - t0 < budget:
     x32 = x.float().numpy()
     fam = lib.btk_kernel_family(m, n, k, b, kb, DTC[dn], 0 if asg == btk.Assignment.INTERLEAVED else 1, n)
     fams[fam] = fams.get(fam, 0) + 1
-    r = btk.approx_topk(x.cuda(), k, btk.BucketScheme(b, kb, asg))
+    xd = x.cuda()
+    if rng.random() < 0.35:  # prepared op, BTK_INPUT_READY, launched right behind another launch
+        op = btk.ApproxTopK(m, n, k, btk.BucketScheme(b, kb, asg), dtype=xd.dtype, device=xd.device,
+                            inputs_ready=True)
+        other = torch.randn_like(xd, dtype=torch.float32).to(xd.dtype)
+        op.launch(other)
+        op.launch(xd)
+        r = btk.TopKResult(values=op.values.clone(), indices=op.indices.clone())
+    else:
+        r = btk.approx_topk(xd, k, btk.BucketScheme(b, kb, asg))
     wv, wi = O.approx_topk(x32, k, b, kb, assignment=O.INTERLEAVED if asg == btk.Assignment.INTERLEAVED else O.CONTIGUOUS)
     gi = r.indices.cpu().numpy()
     gv = r.values.float().cpu().numpy()
