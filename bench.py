@@ -577,6 +577,8 @@ def main():
             "note": "same graph without BTK_INPUT_READY: every launch waits for its predecessor "
                     "before its first read (the contract when the input is produced by the previous kernel)"}
         context["read_probe_ceiling"] = probe_ceiling(cfg)
+        context["read_probe_note"] = ("a plain LDG read-only kernel per launch (tools/probe/readprobe.cu); "
+                                      "the TMA-ring fused kernels can exceed it with BTK_INPUT_READY launches")
 
     scaling_rec = None
     if not args.no_scaling_record and cfg != "cfg5":
@@ -609,7 +611,9 @@ def main():
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": ncu_traffic(cfg), "peak_source": peak_src,
                          "bytes_per_launch": local_bytes,
-                         "bytes_rule": "m*(n*vb + k*(vb+8)) per launch (reference bench.py:154)"},
+                         "bytes_rule": "m*(n*vb + k*(vb+8)) per launch (reference bench.py:154)",
+                         "note": "peak is the measured COPY bandwidth (read+write); a read-dominated stream "
+                                 "runs above it on HBM3e (nominal 8 TB/s), hence frac > 1 on cfg1/cfg3"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(K * launches_per_step),
